@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 D-ADMM hot path (arXiv 1708.07954 data-parallel core).
+
+Metric (BASELINE.json): ADMM observation-updates/sec = l x rounds / time, one
+"step" = one ADMM round (local solve + camera/point consensus + dual update,
+with the round's metrics fused) over the whole synthetic scene.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--loss l2|huber]
+  python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+
+value    : device-timed (CUDA events on the solver stream) K rounds, inputs
+           resident in HBM; the state (~5 GB at config 5) is far larger than
+           L2, so no flush is needed between rounds.
+e2e      : the same metric through the C-ABI with host buffers: create (H2D of
+           the problem + device index build) + K rounds (trace D2H each round)
+           + consensus D2H, wall clock around the synchronous calls.
+roofline : the dominant kernel's achieved vs peak.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADMM observation-updates/sec"
+UNIT = "obs-updates/s"
+CONFIG_ROUNDS = {1: 50, 2: 100, 3: 50, 4: 50, 5: 50}
+CONFIG_NAMES = {1: "config1-tiny-ring", 2: "config2-medium-hemisphere", 3: "config3-outlier-spiral",
+                4: "config4-large-sparse-grid", 5: "config5-scaling-sweep-8-clusters"}
+
+# Algorithmic-work model (Woodbury variant):
+# transcendentals, div and sqrt count as one flop each.
+GN_FLOPS = {"jac": 312, "trial": 190, "acc": 38}
+LBFGS_FLOPS = {"grad": 175, "value": 95, "dir": 18, "dir_pair": 72, "pair": 100}
+# Compulsory HBM bytes per observation per kernel (DESIGN.md §HBM layout).
+BYTES_PER_OBS = {"local": 276.0, "camera": 144.0, "point": 92.0}
+BYTES_PER_POINT = {"point": 48.0 + 8.0}
+BYTES_PER_CAMERA = {"local": 64.0, "camera": 128.0 + 64.0}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "50"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flops_of(stats, loss):
+    if loss == "l2":
+        return (GN_FLOPS["jac"] * stats["n_jacobian"] + GN_FLOPS["trial"] * stats["n_trial"] +
+                GN_FLOPS["acc"] * stats["n_accept"])
+    return (LBFGS_FLOPS["grad"] * stats["n_jacobian"] + LBFGS_FLOPS["value"] * stats["n_trial"] +
+            LBFGS_FLOPS["dir"] * stats["n_direction"] +
+            LBFGS_FLOPS["dir_pair"] * stats["n_pairs_used"] + LBFGS_FLOPS["pair"] * stats["n_accept"])
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def sample_problem(scene, target_obs):
+    """Bounded sample of the same workload: cameras [0, C) and every
+    observation of them (points renumbered). Returns arrays for the oracle."""
+    p = scene.problem
+    counts = np.bincount(p.obs_cam, minlength=p.num_cameras)
+    cum = np.cumsum(counts)
+    C = int(min(p.num_cameras, max(1, np.searchsorted(cum, target_obs) + 1)))
+    sel = p.obs_cam < C
+    pts, inv = np.unique(p.obs_pt[sel], return_inverse=True)
+    return dict(cam_pose=p.cam_pose[:C], cam_f=p.cam_f[:C], points=p.points[pts],
+                obs_cam=p.obs_cam[sel], obs_pt=inv.astype(np.int32), obs_uv=p.obs_uv[sel],
+                init_pose=scene.init.cam_pose[:C], init_pts=scene.init.points[pts],
+                cameras=C, l=int(sel.sum()))
+
+
+def oracle_rounds(sample, loss, workers, rounds, warmup=0):
+    """Runs the CPU restatement of the reference (oracle/) on the sample;
+    returns per-round wall_ms in the reference's own timed scope
+    (local+consensus+dual, admm_solver.cpp:438-443)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    op = O.Problem.create(sample["cam_pose"], sample["cam_f"], sample["points"],
+                          sample["obs_cam"], sample["obs_pt"], sample["obs_uv"])
+    solver = O.AdmmSolver(op, sample["init_pose"], sample["cam_f"], sample["init_pts"],
+                          workers=workers, loss=1 if loss == "huber" else 0,
+                          max_iters=warmup + rounds + 1)
+    ms = []
+    for k in range(warmup + rounds):
+        rec = solver.iterate()
+        if k >= warmup:
+            ms.append(rec["wall_ms"])
+    return ms
+
+
+def cpu_sample_for(scene, loss, workers, budget_s):
+    """Size a sample so one oracle round takes about budget_s on `workers`."""
+    probe = sample_problem(scene, 4000)
+    ms = oracle_rounds(probe, loss, workers, 2)
+    per_obs_s = (max(ms) / 1e3) / probe["l"]
+    return sample_problem(scene, int(max(4000, budget_s / max(per_obs_s, 1e-9))))
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    import paper_1708_07954_b200 as P
+    scene = P.generate_config_scene(args.config, args.seed)
+    workers = os.cpu_count() or 1
+    budget = max(0.05, min(2.0, 150.0 / max(1, args.steps + args.warmup)))
+    sample = cpu_sample_for(scene, args.loss, workers, budget)
+    ms = oracle_rounds(sample, args.loss, workers, args.steps, args.warmup)
+    total_s = sum(ms) / 1e3
+    value = sample["l"] * args.steps / total_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, DESIGN.md §Inputs)",
+        "config": config_block(args, scene),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"cameras [0,{sample['cameras']}) of the scene, "
+                                   f"{sample['l']} observations, one ADMM round per step, "
+                                   f"timed scope local+consensus+dual (admm_solver.cpp:438-443)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(args, scene):
+    p = scene.problem
+    return {"workload": CONFIG_NAMES[args.config], "config_id": args.config,
+            "cameras": int(p.num_cameras), "points": int(p.num_points),
+            "observations": int(p.num_observations), "loss": args.loss,
+            "rounds_per_solve": args.steps, "seed": args.seed,
+            "l2_flush": "not needed: per-round state > 126 MB L2",
+            "parallelism": f"camera-sharded x{args.gpus}" if args.gpus > 1 else "single-gpu"}
+
+
+def our_arm(args, rank, world, local_rank):
+    import torch
+    import paper_1708_07954_b200 as P
+    from paper_1708_07954_b200 import _capi  # noqa: F401
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    scene = P.generate_config_scene(args.config, args.seed)
+    p = scene.problem
+    L = p.num_observations
+    loss = P.LossKind.huber(1.0) if args.loss == "huber" else P.LossKind.squared_l2()
+
+    def opts(rounds):
+        return P.AdmmOptions(misfit_loss=loss, max_iters=rounds, device=dev)
+
+    # ---------------- e2e through the C-ABI from pinned host buffers
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t.numpy()
+
+    hp = P.Problem(pinned(p.obs_cam), pinned(p.obs_pt), pinned(p.obs_uv), pinned(p.cam_pose),
+                   pinned(p.cam_f), pinned(p.points))
+    hinit = P.ParamState(pinned(scene.init.cam_pose), pinned(scene.init.cam_f),
+                         pinned(scene.init.points))
+    # warm the context/module once (untimed)
+    w = P.AdmmSolver(hp, hinit, opts(1))
+    w.run()
+    w.close()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s_e2e = P.AdmmSolver(hp, hinit, opts(args.steps))
+    trace = s_e2e.run()
+    final = s_e2e.consensus()
+    t_e2e = time.perf_counter() - t0
+    s_e2e.close()
+    h2d = (p.obs_cam.nbytes + p.obs_pt.nbytes + p.obs_uv.nbytes + p.cam_pose.nbytes +
+           p.cam_f.nbytes + p.points.nbytes + scene.init.cam_pose.nbytes +
+           scene.init.cam_f.nbytes + scene.init.points.nbytes)
+    d2h = (final.cam_pose.nbytes + final.cam_f.nbytes + final.points.nbytes +
+           len(trace) * 96)
+    e2e_value = L * args.steps / t_e2e
+
+    # ---------------- device-timed rounds, inputs resident
+    solver = P.AdmmSolver(p, scene.init, opts(10 ** 9))
+    for _ in range(args.warmup):
+        solver.enqueue_round()
+    solver.synchronize()
+    solver.reset()
+    solver.reset_stats()
+    solver.set_profiling(True)
+    stream = torch.cuda.ExternalStream(solver.stream_handle(), device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            solver.enqueue_round()
+        e1.record(stream)
+        solver.synchronize()
+        torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    stats = solver.round_stats()
+    last = solver.iterate()  # one more round with the metrics read back (untimed)
+    value = L * world * args.steps / (ms_total / 1e3)
+
+    # ---------------- roofline
+    peaks = measured_peaks()
+    fp64_peak = P.admm.measure_fp64_peak(dev)
+    hbm_peak = peaks.get("hbm_gbs")
+    kernels = {}
+    ncam, npt = p.num_cameras, p.num_points
+    for name, key in (("local", "ms_local"), ("camera", "ms_camera"), ("point", "ms_point")):
+        ms = stats[key] / args.steps
+        byts = BYTES_PER_OBS[name] * L + BYTES_PER_POINT.get(name, 0) * npt + \
+            BYTES_PER_CAMERA.get(name, 0) * ncam
+        kernels[name] = {"ms": ms, "share": stats[key] / max(ms_total, 1e-9),
+                         "gbs": byts / (ms / 1e3) / 1e9,
+                         "frac_hbm": (byts / (ms / 1e3) / 1e9) / hbm_peak if hbm_peak else None}
+    fl = flops_of(stats, args.loss) / args.steps
+    kernels["local"]["tflops"] = fl / (kernels["local"]["ms"] / 1e3) / 1e12
+    kernels["local"]["frac_fp64"] = kernels["local"]["tflops"] / fp64_peak
+    kernels["local"]["flops_per_obs"] = fl / L
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    if dom == "local":
+        roof = {"kernel": "k_local (K1 local solve)", "bound": "fp64",
+                "achieved": kernels["local"]["tflops"], "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": kernels["local"]["frac_fp64"], "traffic": None,
+                "peak_source": "measured on this device by dbag_measure_fp64_peak (DFMA probe); "
+                               "MEASURED_PEAKS.json has no FP64 figure",
+                "hbm_frac_same_kernel": kernels["local"]["frac_hbm"]}
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["gbs"], "peak": hbm_peak,
+                "unit": "GB/s", "frac": kernels[dom]["frac_hbm"], "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        workers = os.cpu_count() or 1
+        sample = cpu_sample_for(scene, args.loss, workers, 3.0)
+        ms = oracle_rounds(sample, args.loss, workers, 3)
+        cpu = {"value": sample["l"] * 3 / (sum(ms) / 1e3), "unit": UNIT, "cores": workers,
+               "kind": "port",
+               "sample": f"cameras [0,{sample['cameras']}) of the same scene, {sample['l']} "
+                         f"observations, 3 ADMM rounds, reference timed scope "
+                         f"(local+consensus+dual), oracle/ restatement (reference needs "
+                         f"Eigen3, absent)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, DESIGN.md §Inputs)",
+            "config": config_block(args, scene),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
+                    "d2h_bytes_per_step": d2h / args.steps,
+                    "scope": f"dbag_create (H2D + device index build) + {args.steps} rounds "
+                             f"(record D2H each) + consensus D2H, wall clock"},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu,
+            "clocks": clocks.summary(), "gpu_launches": 4 * args.steps,
+            "counters": {k: stats[k] for k in ("n_jacobian", "n_trial", "n_accept",
+                                               "n_direction", "n_pairs_used")},
+            "last_round": {k: last[k] for k in ("iter", "mean_reproj_err", "max_primal_x",
+                                                "max_primal_y", "max_dual_x", "max_dual_y")},
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--loss", choices=["l2", "huber"], default="l2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = CONFIG_ROUNDS[args.config]
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local_rank = env_rank()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    return our_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

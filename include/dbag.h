@@ -1,0 +1,218 @@
+/*
+ * dbag.h — C-ABI of the B200-native D-ADMM bundle-adjustment core
+ * (arXiv 1708.07954, data-parallel hot path). Plain C: fixed-width integers,
+ * doubles, opaque handles; no CUDA or torch types cross this boundary.
+ *
+ * Each entry point replaces one call of the reference C++ API
+ * (/root/reference/proj/include/dba/...), cited beside it. A C++ drop-in
+ * wrapper with the reference's class and exception names is in dbag.hpp.
+ *
+ * Conventions (mirroring the reference):
+ *  - Every call is synchronous: it returns after the device work finished,
+ *    as the reference returns after the round (admm_solver.cpp:437-460).
+ *  - Problem arrays are caller-owned only for the duration of dbag_create;
+ *    the handle keeps device copies (the reference holds `const Problem&`,
+ *    admm_solver.hpp:130 — here the caller may free them after create).
+ *  - Errors are status codes (dbag_status) instead of the reference's
+ *    exception hierarchy (errors.hpp:9-72); the message and, for
+ *    DepthBelowGuard, the offending (point, camera) come from
+ *    dbag_last_error / dbag_last_error_info (thread-local).
+ *  - Observation-indexed per-copy state is in BLOCK ORDER: observations
+ *    sorted by (cam_id, point_id) — the reference's partition() order for
+ *    (1,1) blocks (admm_solver.cpp:19-27). dbag_get_block_order maps block
+ *    index -> input observation index.
+ *  - A handle is single-threaded (admm_solver.hpp:74 "not re-entrant").
+ */
+#ifndef DBAG_H_
+#define DBAG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBAG_ABI_VERSION 1
+
+/* errors.hpp:9-72 -> status codes */
+typedef enum {
+  DBAG_OK = 0,
+  DBAG_ERR_VALIDATION = 1,      /* ValidationError                       */
+  DBAG_ERR_SIZE_MISMATCH = 2,   /* SizeMismatch                          */
+  DBAG_ERR_DEPTH_BELOW_GUARD = 3, /* DepthBelowGuard{depth,point,cam}    */
+  DBAG_ERR_SINGULAR = 4,        /* SingularSystem                        */
+  DBAG_ERR_CUDA = 5,            /* device failure (no reference analogue) */
+  DBAG_ERR_NCCL = 6,            /* collective failure                    */
+  DBAG_ERR_INDEX_OUT_OF_RANGE = 7, /* IndexOutOfRange                    */
+  DBAG_ERR_DUPLICATE_OBSERVATION = 8, /* DuplicateObservation            */
+  DBAG_ERR_UNSUPPORTED = 9,     /* valid for the reference, not built here */
+  DBAG_ERR_GENERIC = 10         /* Error (e.g. "local block N: ...")     */
+} dbag_status;
+
+typedef enum { DBAG_LOSS_SQUARED_L2 = 0, DBAG_LOSS_HUBER = 1 } dbag_loss; /* losses.hpp:13-29 */
+
+/* A problem in SoA form (problem.hpp:11-56: Observation, CameraParams,
+ * ScenePoint). Camera pose order is (alpha, beta, gamma, t1, t2, t3) with
+ * R = Rz(gamma) Ry(beta) Rx(alpha) (geometry.hpp:20-47). */
+typedef struct {
+  int32_t num_cameras;   /* m */
+  int32_t num_points;    /* n */
+  int64_t num_obs;       /* l (< 2^31) */
+  const int32_t* obs_cam;  /* [l] */
+  const int32_t* obs_pt;   /* [l] */
+  const double* obs_uv;    /* [l][2] pixels */
+  const double* cam_pose;  /* [m][6] nominal record (validated only) */
+  const double* cam_f;     /* [m]    nominal focal (validated only)  */
+  const double* points;    /* [n][3] nominal record (validated), nullable */
+} dbag_problem_view;
+
+/* A ParamState (problem.hpp:36-41). f rides along, never optimised. */
+typedef struct {
+  int32_t num_cameras;
+  int32_t num_points;
+  const double* cam_pose;  /* [m][6] */
+  const double* cam_f;     /* [m]; NULL -> the problem's cam_f */
+  const double* points;    /* [n][3] */
+} dbag_param_view;
+
+/* AdmmOptions + InnerOptions + ProjectionGuard + BlockConfig
+ * (admm_solver.hpp:15-33, local_opt.hpp:11-19, geometry.hpp:50-52). */
+typedef struct {
+  double rho_x, rho_y;
+  int32_t max_iters;
+  double primal_tol;
+  int32_t stop_on_primal;
+  int32_t loss;            /* dbag_loss */
+  double huber_delta;
+  int32_t inner_max_iters;
+  double grad_tol, step_tol;
+  int32_t lbfgs_memory;    /* 1..DBAG_MAX_LBFGS_MEMORY */
+  double armijo_c, backtrack;
+  int32_t max_line_search;
+  double eps_depth;
+  int32_t workers;         /* validated >= 1 (reference semantics); unused on GPU */
+  int32_t points_per_block, cameras_per_block; /* only (1,1) is built */
+  int32_t device;          /* CUDA device ordinal */
+} dbag_options;
+
+#define DBAG_MAX_LBFGS_MEMORY 8
+
+/* IterationRecord (trace.hpp:12-21) + appended extension fields. */
+typedef struct {
+  int32_t iter;
+  double mean_reproj_err;
+  double max_primal_x, max_primal_y;
+  double camera_mse, point_mse;   /* NaN without a reference */
+  double wall_ms;                 /* device time of local+consensus+dual */
+  int64_t comm_floats;
+  /* extensions: dual residuals rho*max||xbar^{k+1}-xbar^k|| */
+  double max_dual_x, max_dual_y;
+  double sum_reproj_err;          /* sum ||z - pi(xbar, ybar)|| (mean * l) */
+} dbag_iteration_record;
+
+/* Device-event counters for the FLOP model. */
+typedef struct {
+  uint64_t n_jacobian;   /* Jacobian/gradient evaluations */
+  uint64_t n_trial;      /* trial residual / value evaluations */
+  uint64_t n_accept;     /* accepted steps */
+  uint64_t n_direction;  /* L-BFGS two-loop directions */
+  uint64_t n_pairs_used; /* L-BFGS: sum of history sizes over directions */
+  double ms_local, ms_camera, ms_point, ms_final; /* last enqueued round */
+} dbag_round_stats;
+
+typedef struct dbag_solver dbag_solver;
+
+int32_t dbag_abi_version(void);
+const char* dbag_last_error(void);
+/* DepthBelowGuard payload (errors.hpp:52-63); -1 when not applicable.
+ * block: offending block index for "local block N" errors. */
+void dbag_last_error_info(int32_t* point_id, int32_t* cam_id, double* depth, int64_t* block);
+
+void dbag_options_default(dbag_options* o); /* AdmmOptions{} defaults */
+
+/* Problem::create + AdmmSolver::AdmmSolver (problem.cpp:66-96,
+ * admm_solver.cpp:103-142): validates, uploads, builds the block order and
+ * copy maps on the device (partition, admm_solver.cpp:14-72; copy maps
+ * :126-140; build_visibility, problem.cpp:12-64), copies = init, duals = 0. */
+int dbag_create(const dbag_problem_view* problem, const dbag_param_view* init,
+                const dbag_options* opts, dbag_solver** out);
+void dbag_destroy(dbag_solver* h);
+
+/* Phases (admm_solver.cpp:144-357). */
+int dbag_local_update(dbag_solver* h, int64_t block); /* local_update(int) */
+int dbag_local_update_all(dbag_solver* h);           /* local_update_all() */
+int dbag_consensus_update(dbag_solver* h);           /* consensus_update() */
+int dbag_dual_update(dbag_solver* h);                /* dual_update()      */
+
+/* Reference state for the MSE columns of iterate()/run() (the reference
+ * passes `const ParamState*` per call, admm_solver.hpp:97-100). NULL clears. */
+int dbag_set_reference(dbag_solver* h, const dbag_param_view* ref);
+/* iterate(const ParamState*) (admm_solver.cpp:437-460); with_reference != 0
+ * fills camera_mse/point_mse against the dbag_set_reference state. */
+int dbag_iterate(dbag_solver* h, int32_t with_reference, dbag_iteration_record* out);
+/* run(const ParamState*) (admm_solver.cpp:462-474): rounds until max_iters
+ * (or stop_on_primal). Writes min(cap, rounds) records; *n_out = rounds. */
+int dbag_run(dbag_solver* h, int32_t with_reference, dbag_iteration_record* trace, int64_t cap,
+             int64_t* n_out);
+
+/* state() queries (admm_solver.hpp:102-108). */
+int dbag_get_consensus(dbag_solver* h, double* cam_pose /*[m][6]*/, double* cam_f /*[m], nullable*/,
+                       double* points /*[n][3]*/);
+int dbag_set_consensus(dbag_solver* h, const double* cam_pose, const double* points);
+int dbag_get_copies(dbag_solver* h, double* local_points /*[l][3]*/, double* local_cams /*[l][6]*/,
+                    double* dual_r /*[l][3]*/, double* dual_s /*[l][6]*/); /* block order */
+int dbag_set_copies(dbag_solver* h, const double* local_points, const double* local_cams,
+                    const double* dual_r, const double* dual_s);
+int32_t dbag_iteration(dbag_solver* h);
+int64_t dbag_num_blocks(dbag_solver* h);
+int dbag_get_block_order(dbag_solver* h, int32_t* obs_ids /*[l]*/); /* blocks()[b].obs_ids[0] */
+
+/* Result/objective queries (admm_solver.hpp:110-127). */
+int dbag_max_primal(dbag_solver* h, double* max_x, double* max_y);
+int dbag_dual_sums(dbag_solver* h, double* point_sums /*[n][3]*/, double* cam_sums /*[m][6]*/);
+int dbag_block_objective(dbag_solver* h, int64_t block, double* out);
+int64_t dbag_ops_per_iteration(dbag_solver* h);  /* ops_per_iteration() */
+int64_t dbag_comm_floats(dbag_solver* h);        /* comm_floats_per_iteration() */
+
+/* problem.hpp:59-85 at the current consensus. */
+int dbag_mean_reprojection_error(dbag_solver* h, double* out); /* throws-variant semantics */
+int dbag_total_squared_error(dbag_solver* h, double* out);
+
+/* Measurement hooks (no reference analogue): enqueue one full round
+ * (local+consensus+dual+metrics) on the handle's stream without waiting;
+ * dbag_stream returns the cudaStream_t as an opaque pointer. */
+int dbag_enqueue_round(dbag_solver* h);
+int dbag_reset(dbag_solver* h); /* restart from the init state: copies = init, duals = 0 */
+void* dbag_stream(dbag_solver* h);
+int dbag_synchronize(dbag_solver* h);
+int dbag_set_profiling(dbag_solver* h, int32_t on); /* per-round kernel events, summed */
+int dbag_get_round_stats(dbag_solver* h, dbag_round_stats* out); /* counters since reset */
+int dbag_reset_stats(dbag_solver* h);
+/* FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA): the FP64
+ * roofline denominator, which MEASURED_PEAKS.json does not carry. */
+int dbag_measure_fp64_peak(int32_t device, double* tflops);
+
+/* Synthetic scenes of BASELINE.json configs 1-5 (host C++, deterministic in
+ * seed). Two-phase: size query, then fill. scale in (0,1]
+ * shrinks points/cameras proportionally for bounded samples. */
+typedef struct {
+  int32_t config;        /* 1..5 */
+  uint64_t seed;
+  double scale;          /* 1.0 = the BASELINE size */
+  int32_t num_cameras, num_points;
+  int64_t num_obs;
+  double sigma_pixel, outlier_frac, sigma_init;
+} dbag_scene_info;
+typedef struct dbag_scene dbag_scene;
+int dbag_scene_generate(int32_t config, uint64_t seed, double scale, dbag_scene** out,
+                        dbag_scene_info* info);
+/* gt_* = ground truth; init_* = perturb(gt, sigma_init); obs in emission order */
+int dbag_scene_fetch(dbag_scene* s, int32_t* obs_cam, int32_t* obs_pt, double* obs_uv,
+                     double* gt_pose, double* cam_f, double* gt_points, double* init_pose,
+                     double* init_points);
+void dbag_scene_destroy(dbag_scene* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBAG_H_ */

@@ -1,0 +1,133 @@
+"""ctypes binding of include/dbag.h (the product C-ABI, libdbag.so).
+
+Loads the in-tree libdbag.so and fails loudly when it is missing: there is no
+CPU fallback anywhere in the product path."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdbag.so")
+
+DPTR = C.POINTER(C.c_double)
+I32P = C.POINTER(C.c_int32)
+I64P = C.POINTER(C.c_int64)
+
+
+class ProblemView(C.Structure):
+    _fields_ = [("num_cameras", C.c_int32), ("num_points", C.c_int32), ("num_obs", C.c_int64),
+                ("obs_cam", I32P), ("obs_pt", I32P), ("obs_uv", DPTR), ("cam_pose", DPTR),
+                ("cam_f", DPTR), ("points", DPTR)]
+
+
+class ParamView(C.Structure):
+    _fields_ = [("num_cameras", C.c_int32), ("num_points", C.c_int32), ("cam_pose", DPTR),
+                ("cam_f", DPTR), ("points", DPTR)]
+
+
+class Options(C.Structure):
+    _fields_ = [("rho_x", C.c_double), ("rho_y", C.c_double), ("max_iters", C.c_int32),
+                ("primal_tol", C.c_double), ("stop_on_primal", C.c_int32), ("loss", C.c_int32),
+                ("huber_delta", C.c_double), ("inner_max_iters", C.c_int32),
+                ("grad_tol", C.c_double), ("step_tol", C.c_double), ("lbfgs_memory", C.c_int32),
+                ("armijo_c", C.c_double), ("backtrack", C.c_double),
+                ("max_line_search", C.c_int32), ("eps_depth", C.c_double),
+                ("workers", C.c_int32), ("points_per_block", C.c_int32),
+                ("cameras_per_block", C.c_int32), ("device", C.c_int32)]
+
+
+class IterationRecord(C.Structure):
+    _fields_ = [("iter", C.c_int32), ("mean_reproj_err", C.c_double),
+                ("max_primal_x", C.c_double), ("max_primal_y", C.c_double),
+                ("camera_mse", C.c_double), ("point_mse", C.c_double), ("wall_ms", C.c_double),
+                ("comm_floats", C.c_int64), ("max_dual_x", C.c_double),
+                ("max_dual_y", C.c_double), ("sum_reproj_err", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class RoundStats(C.Structure):
+    _fields_ = [("n_jacobian", C.c_uint64), ("n_trial", C.c_uint64), ("n_accept", C.c_uint64),
+                ("n_direction", C.c_uint64), ("n_pairs_used", C.c_uint64),
+                ("ms_local", C.c_double), ("ms_camera", C.c_double), ("ms_point", C.c_double),
+                ("ms_final", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class SceneInfo(C.Structure):
+    _fields_ = [("config", C.c_int32), ("seed", C.c_uint64), ("scale", C.c_double),
+                ("num_cameras", C.c_int32), ("num_points", C.c_int32), ("num_obs", C.c_int64),
+                ("sigma_pixel", C.c_double), ("outlier_frac", C.c_double),
+                ("sigma_init", C.c_double)]
+
+
+H = C.c_void_p
+
+# name -> (restype, argtypes); every symbol declared in include/dbag.h
+SIGNATURES = {
+    "dbag_abi_version": (C.c_int32, []),
+    "dbag_last_error": (C.c_char_p, []),
+    "dbag_last_error_info": (None, [I32P, I32P, DPTR, I64P]),
+    "dbag_options_default": (None, [C.POINTER(Options)]),
+    "dbag_create": (C.c_int, [C.POINTER(ProblemView), C.POINTER(ParamView), C.POINTER(Options),
+                              C.POINTER(H)]),
+    "dbag_destroy": (None, [H]),
+    "dbag_local_update": (C.c_int, [H, C.c_int64]),
+    "dbag_local_update_all": (C.c_int, [H]),
+    "dbag_consensus_update": (C.c_int, [H]),
+    "dbag_dual_update": (C.c_int, [H]),
+    "dbag_set_reference": (C.c_int, [H, C.POINTER(ParamView)]),
+    "dbag_iterate": (C.c_int, [H, C.c_int32, C.POINTER(IterationRecord)]),
+    "dbag_run": (C.c_int, [H, C.c_int32, C.POINTER(IterationRecord), C.c_int64, I64P]),
+    "dbag_get_consensus": (C.c_int, [H, DPTR, DPTR, DPTR]),
+    "dbag_set_consensus": (C.c_int, [H, DPTR, DPTR]),
+    "dbag_get_copies": (C.c_int, [H, DPTR, DPTR, DPTR, DPTR]),
+    "dbag_set_copies": (C.c_int, [H, DPTR, DPTR, DPTR, DPTR]),
+    "dbag_iteration": (C.c_int32, [H]),
+    "dbag_num_blocks": (C.c_int64, [H]),
+    "dbag_get_block_order": (C.c_int, [H, I32P]),
+    "dbag_max_primal": (C.c_int, [H, DPTR, DPTR]),
+    "dbag_dual_sums": (C.c_int, [H, DPTR, DPTR]),
+    "dbag_block_objective": (C.c_int, [H, C.c_int64, DPTR]),
+    "dbag_ops_per_iteration": (C.c_int64, [H]),
+    "dbag_comm_floats": (C.c_int64, [H]),
+    "dbag_mean_reprojection_error": (C.c_int, [H, DPTR]),
+    "dbag_total_squared_error": (C.c_int, [H, DPTR]),
+    "dbag_enqueue_round": (C.c_int, [H]),
+    "dbag_reset": (C.c_int, [H]),
+    "dbag_stream": (C.c_void_p, [H]),
+    "dbag_synchronize": (C.c_int, [H]),
+    "dbag_set_profiling": (C.c_int, [H, C.c_int32]),
+    "dbag_get_round_stats": (C.c_int, [H, C.POINTER(RoundStats)]),
+    "dbag_reset_stats": (C.c_int, [H]),
+    "dbag_measure_fp64_peak": (C.c_int, [C.c_int32, DPTR]),
+    "dbag_scene_generate": (C.c_int, [C.c_int32, C.c_uint64, C.c_double, C.POINTER(H),
+                                      C.POINTER(SceneInfo)]),
+    "dbag_scene_fetch": (C.c_int, [H, I32P, I32P, DPTR, DPTR, DPTR, DPTR, DPTR, DPTR]),
+    "dbag_scene_destroy": (None, [H]),
+}
+
+_lib = None
+
+
+def load(build_if_missing=True):
+    """Load libdbag.so (building it in-tree when absent and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        if not build_if_missing:
+            raise ImportError(f"libdbag.so missing at {LIB_PATH}; run __graft_entry__.build()")
+        from . import build as _b
+        _b.build()
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,439 @@
+"""Host-side mirror of the reference solver API over the B200 C-ABI.
+
+Mirrors proj/include/dba/{admm_solver,problem,trace,errors}.hpp: the same
+class and method names, argument meaning and exception types, so tests read
+like the reference's own (proj/tests/test_admm_solver.cpp). Every compute call
+goes through libdbag.so (include/dbag.h); nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+
+# ---- errors (proj/include/dba/errors.hpp:9-72) -------------------------------
+
+
+class Error(RuntimeError):
+    """dba::Error."""
+
+
+class ValidationError(Error):
+    """dba::ValidationError."""
+
+
+class SizeMismatch(ValidationError):
+    pass
+
+
+class IndexOutOfRange(ValidationError):
+    pass
+
+
+class DuplicateObservation(ValidationError):
+    pass
+
+
+class DepthBelowGuard(Error):
+    def __init__(self, msg, depth=0.0, point_id=-1, cam_id=-1):
+        super().__init__(msg)
+        self.depth, self.point_id, self.cam_id = depth, point_id, cam_id
+
+
+class SingularSystem(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / NCCL failure (no reference analogue)."""
+
+
+class Unsupported(Error):
+    """Valid for the reference but not built on the device (e.g. (pi,kappa) > 1 blocks)."""
+
+
+_STATUS = {1: ValidationError, 2: SizeMismatch, 3: DepthBelowGuard, 4: SingularSystem,
+           5: DeviceError, 6: DeviceError, 7: IndexOutOfRange, 8: DuplicateObservation,
+           9: Unsupported, 10: Error}
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    lib = _capi.load()
+    msg = lib.dbag_last_error().decode()
+    pt, cam, blk = C.c_int32(), C.c_int32(), C.c_int64()
+    depth = C.c_double()
+    lib.dbag_last_error_info(C.byref(pt), C.byref(cam), C.byref(depth), C.byref(blk))
+    cls = _STATUS.get(rc, Error)
+    if cls is DepthBelowGuard:
+        raise DepthBelowGuard(msg, depth.value, pt.value, cam.value)
+    err = cls(msg)
+    err.block = blk.value
+    raise err
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(_capi.DPTR)
+
+
+def _ip(a):
+    return a.ctypes.data_as(_capi.I32P)
+
+
+# ---- data model (proj/include/dba/problem.hpp, geometry.hpp) -------------------
+
+
+@dataclass
+class ParamState:
+    """problem.hpp:36-41. cam_pose rows are (alpha, beta, gamma, t1, t2, t3)."""
+    cam_pose: np.ndarray
+    cam_f: np.ndarray
+    points: np.ndarray
+
+    def copy(self):
+        return ParamState(self.cam_pose.copy(), self.cam_f.copy(), self.points.copy())
+
+    def _view(self):
+        self.cam_pose = _f64(self.cam_pose, (-1, 6))
+        self.cam_f = _f64(self.cam_f)
+        self.points = _f64(self.points, (-1, 3))
+        return _capi.ParamView(len(self.cam_f), len(self.points), _dp(self.cam_pose),
+                               _dp(self.cam_f), _dp(self.points))
+
+
+@dataclass
+class Problem:
+    """problem.hpp:44-56 in SoA form: observations (cam_id, point_id, z) and the
+    nominal camera/point record. Validation happens on the device at solver
+    construction (Problem::create + build_visibility semantics)."""
+    obs_cam: np.ndarray
+    obs_pt: np.ndarray
+    obs_uv: np.ndarray
+    cam_pose: np.ndarray
+    cam_f: np.ndarray
+    points: np.ndarray
+
+    @classmethod
+    def create(cls, cam_pose, cam_f, points, obs_cam, obs_pt, obs_uv):
+        return cls(np.ascontiguousarray(obs_cam, np.int32), np.ascontiguousarray(obs_pt, np.int32),
+                   _f64(obs_uv, (-1, 2)), _f64(cam_pose, (-1, 6)), _f64(cam_f), _f64(points, (-1, 3)))
+
+    @property
+    def num_cameras(self):
+        return len(self.cam_f)
+
+    @property
+    def num_points(self):
+        return len(self.points)
+
+    @property
+    def num_observations(self):
+        return len(self.obs_cam)
+
+    def nominal_state(self):
+        return ParamState(self.cam_pose.copy(), self.cam_f.copy(), self.points.copy())
+
+    def _view(self):
+        return _capi.ProblemView(self.num_cameras, self.num_points, self.num_observations,
+                                 _ip(self.obs_cam), _ip(self.obs_pt), _dp(self.obs_uv),
+                                 _dp(self.cam_pose), _dp(self.cam_f), _dp(self.points))
+
+
+@dataclass
+class InnerOptions:
+    """local_opt.hpp:11-19."""
+    max_iters: int = 10
+    grad_tol: float = 1e-8
+    step_tol: float = 1e-10
+    lbfgs_memory: int = 8
+    armijo_c: float = 1e-4
+    backtrack: float = 0.5
+    max_line_search: int = 40
+
+
+SQUARED_L2, HUBER = 0, 1
+
+
+@dataclass
+class LossKind:
+    """losses.hpp:13-29."""
+    type: int = SQUARED_L2
+    delta: float = 1.0
+
+    @staticmethod
+    def squared_l2():
+        return LossKind(SQUARED_L2, 1.0)
+
+    @staticmethod
+    def huber(delta):
+        if not delta > 0.0:
+            raise ValidationError("Huber delta must be > 0")
+        return LossKind(HUBER, delta)
+
+    def is_huber(self):
+        return self.type == HUBER
+
+
+@dataclass
+class AdmmOptions:
+    """admm_solver.hpp:15-25 (+ ProjectionGuard, BlockConfig, device)."""
+    rho_x: float = 1.0
+    rho_y: float = 1.0
+    max_iters: int = 1600
+    primal_tol: float = 1e-6
+    stop_on_primal: bool = False
+    misfit_loss: LossKind = field(default_factory=LossKind)
+    inner: InnerOptions = field(default_factory=InnerOptions)
+    eps_depth: float = 1e-6
+    workers: int = 1
+    points_per_block: int = 1
+    cameras_per_block: int = 1
+    device: int = 0
+
+    def _c(self):
+        o = _capi.Options()
+        _capi.load().dbag_options_default(C.byref(o))
+        o.rho_x, o.rho_y, o.max_iters = self.rho_x, self.rho_y, self.max_iters
+        o.primal_tol, o.stop_on_primal = self.primal_tol, int(self.stop_on_primal)
+        o.loss, o.huber_delta = self.misfit_loss.type, self.misfit_loss.delta
+        i = self.inner
+        o.inner_max_iters, o.grad_tol, o.step_tol = i.max_iters, i.grad_tol, i.step_tol
+        o.lbfgs_memory, o.armijo_c, o.backtrack = i.lbfgs_memory, i.armijo_c, i.backtrack
+        o.max_line_search, o.eps_depth, o.workers = i.max_line_search, self.eps_depth, self.workers
+        o.points_per_block, o.cameras_per_block = self.points_per_block, self.cameras_per_block
+        o.device = self.device
+        return o
+
+
+@dataclass
+class AdmmState:
+    """admm_solver.hpp:57-64 for (1,1) blocks, per-copy arrays in block order."""
+    local_points: np.ndarray
+    local_cameras: np.ndarray
+    dual_r: np.ndarray
+    dual_s: np.ndarray
+    consensus: ParamState
+    iteration: int
+
+
+class AdmmSolver:
+    """dba::AdmmSolver (admm_solver.hpp:75-138) on one B200."""
+
+    def __init__(self, problem: Problem, init: ParamState, opts: AdmmOptions | None = None):
+        self._lib = _capi.load()
+        self.problem = problem
+        self.opts = opts or AdmmOptions()
+        self._h = C.c_void_p()
+        init = init.copy()
+        pv, iv, o = problem._view(), init._view(), self.opts._c()
+        _check(self._lib.dbag_create(C.byref(pv), C.byref(iv), C.byref(o), C.byref(self._h)))
+        self.m, self.n = problem.num_cameras, problem.num_points
+        self.l = problem.num_observations
+        self._ref_key = None
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.dbag_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- phases (admm_solver.cpp:144-357)
+    def local_update(self, block_index):
+        _check(self._lib.dbag_local_update(self._h, block_index))
+
+    def local_update_all(self):
+        _check(self._lib.dbag_local_update_all(self._h))
+
+    def consensus_update(self):
+        _check(self._lib.dbag_consensus_update(self._h))
+
+    def dual_update(self):
+        _check(self._lib.dbag_dual_update(self._h))
+
+    def _use_reference(self, reference):
+        if reference is None:
+            return 0
+        key = (id(reference.cam_pose), id(reference.points))
+        if key != self._ref_key:
+            ref = reference.copy()
+            v = ref._view()
+            _check(self._lib.dbag_set_reference(self._h, C.byref(v)))
+            self._ref_key = key
+        return 1
+
+    def iterate(self, reference: ParamState | None = None):
+        rec = _capi.IterationRecord()
+        _check(self._lib.dbag_iterate(self._h, self._use_reference(reference), C.byref(rec)))
+        return rec.as_dict()
+
+    def run(self, reference: ParamState | None = None):
+        cap = max(1, self.opts.max_iters - self.iteration)
+        trace = (_capi.IterationRecord * cap)()
+        n = C.c_int64()
+        _check(self._lib.dbag_run(self._h, self._use_reference(reference), trace, cap,
+                                  C.byref(n)))
+        return [trace[k].as_dict() for k in range(min(n.value, cap))]
+
+    # ---- state
+    @property
+    def iteration(self):
+        return self._lib.dbag_iteration(self._h)
+
+    def consensus(self) -> ParamState:
+        pose, f, pts = np.zeros((self.m, 6)), np.zeros(self.m), np.zeros((self.n, 3))
+        _check(self._lib.dbag_get_consensus(self._h, _dp(pose), _dp(f), _dp(pts)))
+        return ParamState(pose, f, pts)
+
+    def set_consensus(self, state: ParamState):
+        pose, pts = _f64(state.cam_pose, (-1, 6)), _f64(state.points, (-1, 3))
+        _check(self._lib.dbag_set_consensus(self._h, _dp(pose), _dp(pts)))
+
+    def state(self) -> AdmmState:
+        lp, lc = np.zeros((self.l, 3)), np.zeros((self.l, 6))
+        r, s = np.zeros((self.l, 3)), np.zeros((self.l, 6))
+        _check(self._lib.dbag_get_copies(self._h, _dp(lp), _dp(lc), _dp(r), _dp(s)))
+        return AdmmState(lp, lc, r, s, self.consensus(), self.iteration)
+
+    def set_copies(self, local_points, local_cameras, dual_r, dual_s):
+        a, b = _f64(local_points, (-1, 3)), _f64(local_cameras, (-1, 6))
+        c, d = _f64(dual_r, (-1, 3)), _f64(dual_s, (-1, 6))
+        _check(self._lib.dbag_set_copies(self._h, _dp(a), _dp(b), _dp(c), _dp(d)))
+
+    def blocks(self):
+        """Block order: blocks()[b].obs_ids[0] for (1,1) blocks."""
+        out = np.zeros(self.l, np.int32)
+        _check(self._lib.dbag_get_block_order(self._h, _ip(out)))
+        return out
+
+    # ---- queries (admm_solver.hpp:110-127)
+    def max_primal_residual_points(self):
+        return self._max_primal()[0]
+
+    def max_primal_residual_cameras(self):
+        return self._max_primal()[1]
+
+    def _max_primal(self):
+        x, y = C.c_double(), C.c_double()
+        _check(self._lib.dbag_max_primal(self._h, C.byref(x), C.byref(y)))
+        return x.value, y.value
+
+    def dual_sums(self):
+        p, c = np.zeros((self.n, 3)), np.zeros((self.m, 6))
+        _check(self._lib.dbag_dual_sums(self._h, _dp(p), _dp(c)))
+        return p, c
+
+    def dual_sum_point(self, i):
+        return self.dual_sums()[0][i]
+
+    def dual_sum_camera(self, j):
+        return self.dual_sums()[1][j]
+
+    def block_objective(self, b):
+        out = C.c_double()
+        _check(self._lib.dbag_block_objective(self._h, b, C.byref(out)))
+        return out.value
+
+    def ops_per_iteration(self):
+        return self._lib.dbag_ops_per_iteration(self._h)
+
+    def comm_floats_per_iteration(self):
+        return self._lib.dbag_comm_floats(self._h)
+
+    def mean_reprojection_error(self):
+        out = C.c_double()
+        _check(self._lib.dbag_mean_reprojection_error(self._h, C.byref(out)))
+        return out.value
+
+    def total_squared_error(self):
+        out = C.c_double()
+        _check(self._lib.dbag_total_squared_error(self._h, C.byref(out)))
+        return out.value
+
+    # ---- measurement hooks
+    def enqueue_round(self):
+        _check(self._lib.dbag_enqueue_round(self._h))
+
+    def reset(self):
+        """Restart from the init state (copies = init consensus, duals = 0)."""
+        _check(self._lib.dbag_reset(self._h))
+
+    def set_profiling(self, on=True):
+        _check(self._lib.dbag_set_profiling(self._h, int(on)))
+
+    def stream_handle(self):
+        return self._lib.dbag_stream(self._h)
+
+    def synchronize(self):
+        _check(self._lib.dbag_synchronize(self._h))
+
+    def round_stats(self):
+        s = _capi.RoundStats()
+        _check(self._lib.dbag_get_round_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        _check(self._lib.dbag_reset_stats(self._h))
+
+
+def measure_fp64_peak(device=0):
+    """FP64 FMA throughput (TFLOP/s) of the device: the local-solve roofline."""
+    out = C.c_double()
+    _check(_capi.load().dbag_measure_fp64_peak(device, C.byref(out)))
+    return out.value
+
+
+def run_admm(problem, init, opts=None, reference=None):
+    """admm_solver.cpp:476-480 -> (final consensus, trace)."""
+    solver = AdmmSolver(problem, init, opts)
+    trace = solver.run(reference)
+    out = solver.consensus()
+    solver.close()
+    return out, trace
+
+
+# ---- synthetic config scenes (dbag_scene_*) -----------------------------------
+
+
+@dataclass
+class Scene:
+    problem: Problem
+    ground_truth: ParamState
+    init: ParamState
+    info: dict
+
+
+def generate_config_scene(config: int, seed: int = 0, scale: float = 1.0) -> Scene:
+    """BASELINE.json config 1..5; deterministic in seed."""
+    lib = _capi.load()
+    h = C.c_void_p()
+    info = _capi.SceneInfo()
+    _check(lib.dbag_scene_generate(config, seed, scale, C.byref(h), C.byref(info)))
+    try:
+        m, n, l = info.num_cameras, info.num_points, info.num_obs
+        cam, pt = np.zeros(l, np.int32), np.zeros(l, np.int32)
+        uv, gt_pose, f = np.zeros((l, 2)), np.zeros((m, 6)), np.zeros(m)
+        gt_pts, ip, ix = np.zeros((n, 3)), np.zeros((m, 6)), np.zeros((n, 3))
+        _check(lib.dbag_scene_fetch(h, _ip(cam), _ip(pt), _dp(uv), _dp(gt_pose), _dp(f),
+                                    _dp(gt_pts), _dp(ip), _dp(ix)))
+    finally:
+        lib.dbag_scene_destroy(h)
+    prob = Problem(cam, pt, uv, gt_pose, f, gt_pts)
+    d = {k: getattr(info, k) for k, _ in info._fields_}
+    return Scene(prob, ParamState(gt_pose.copy(), f.copy(), gt_pts.copy()),
+                 ParamState(ip, f.copy(), ix), d)

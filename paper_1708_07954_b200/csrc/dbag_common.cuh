@@ -1,0 +1,121 @@
+// dbag_common.cuh — device state layout and fp64 camera math shared by the
+// B200 kernels. See DESIGN.md §HBM layout for the byte budget per observation.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dbag {
+
+// Point-side per-copy record, stored in POINT-MAJOR order (copies of one point
+// contiguous, ascending camera = ascending block order, admm_solver.cpp:126-140).
+// 64 B = two full 32 B sectors: the local solve gathers it once per round, the
+// point consensus pass streams it.
+struct __align__(16) PointRec {
+  double x0, x1, x2;  // local point copy x_i^j
+  double r0;          // dual r_i^j
+  double r1, r2;
+  double u, v;        // observation z (read-only)
+};
+static_assert(sizeof(PointRec) == 64, "PointRec must be 64 B");
+
+// Everything a kernel needs, passed by value (fits the 4 KB param space).
+struct DevState {
+  int64_t L;       // observations == blocks (1,1)
+  int32_t M, N;    // cameras, points
+  // block order (sorted by (cam, pt)): camera-side SoA [12][L] = y(6) | s(6)
+  double* cam_soa;
+  int32_t* blk_cam;   // [L]
+  int32_t* blk_pt;    // [L]
+  int32_t* blk_pos;   // [L] point-major position of block b
+  int32_t* blk_obs;   // [L] input observation index of block b
+  // point-major
+  PointRec* prec;     // [L]
+  int32_t* pm_cam;    // [L] camera of point-major position p
+  int32_t* pt_off;    // [N+1]
+  int32_t* pt_order;  // [N] processing order (by descending track length)
+  int32_t* cam_off;   // [M+1]
+  // consensus
+  double4* xbar;      // [N] (x, y, z, 0)
+  double* ybar;       // [M][8] (alpha, beta, gamma, t0, t1, t2, f, 0)
+  double* camR;       // [M][16] R(9) t(3) f at ybar (for the fused metric)
+  // reference state for the MSE columns
+  double* ref_pose;   // [M][6] or null
+  double* ref_pts;    // [N][3] or null
+  // options
+  double rho_x, rho_y, eps_depth, huber_delta;
+  double grad_tol, step_tol, armijo_c, backtrack;
+  int32_t inner_max_iters, lbfgs_memory, max_line_search, loss;
+  // reductions
+  double* part_pt;        // [gridK2][4] sum_err, max_px, max_dx, infeasible
+  double* cam_stats;      // [M][2] primal_y, dual_y
+  double* part_mse;       // [gridMSE][2]
+  unsigned long long* counters;  // [kCounterStripes][8]
+  int64_t* err_block;     // first block that raised (local_update_all)
+  int64_t* err_obs;       // first infeasible observation (input order)
+  double* record;         // DevRecord
+};
+
+constexpr int kCounterStripes = 64;
+
+// DevRecord layout (doubles)
+enum RecField {
+  kRecSumErr = 0, kRecMaxPx, kRecMaxPy, kRecMaxDx, kRecMaxDy, kRecInfeasible, kRecCamMse,
+  kRecPtMse, kRecFields
+};
+
+// ---------------------------------------------------------------------------
+// Camera model, geometry.cpp:9-99,141-159. R = Rz(g) Ry(b) Rx(a), formed as
+// (Rz*Ry)*Rx like rotation_from_euler (geometry.cpp:62-64), with the
+// structural zeros folded.
+// ---------------------------------------------------------------------------
+struct Trig {
+  double sa, ca, sb, cb, sg, cg;
+};
+
+__device__ __forceinline__ void trig_of(double a, double b, double g, Trig& t) {
+  sincos(a, &t.sa, &t.ca);
+  sincos(b, &t.sb, &t.cb);
+  sincos(g, &t.sg, &t.cg);
+}
+
+__device__ __forceinline__ void rot_of(const Trig& t, double R[9]) {
+  const double m01 = -t.sg, m02 = t.cg * t.sb;
+  const double m11 = t.cg, m12 = t.sg * t.sb;
+  const double m22 = t.cb;
+  R[0] = t.cg * t.cb;
+  R[1] = m01 * t.ca + m02 * t.sa;
+  R[2] = m01 * (-t.sa) + m02 * t.ca;
+  R[3] = t.sg * t.cb;
+  R[4] = m11 * t.ca + m12 * t.sa;
+  R[5] = m11 * (-t.sa) + m12 * t.ca;
+  R[6] = -t.sb;
+  R[7] = m22 * t.sa;
+  R[8] = m22 * t.ca;
+}
+
+// w = R x + t (geometry.cpp:93)
+__device__ __forceinline__ void cam_point(const double R[9], const double* x, const double* t,
+                                          double w[3]) {
+  w[0] = (R[0] * x[0] + R[1] * x[1] + R[2] * x[2]) + t[0];
+  w[1] = (R[3] * x[0] + R[4] * x[1] + R[5] * x[2]) + t[1];
+  w[2] = (R[6] * x[0] + R[7] * x[1] + R[8] * x[2]) + t[2];
+}
+
+// Feasibility test of geometry.cpp:95 (`!(w3 >= eps)` also rejects NaN).
+__device__ __forceinline__ bool feasible(double w2, double eps) { return w2 >= eps; }
+
+// Lower-pass block reduce helpers (deterministic fixed-shape trees).
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace dbag

@@ -1,0 +1,259 @@
+// dbag_local.cuh — K1: the per-observation local solve of one ADMM round.
+//
+// Restates AdmmSolver::local_update for (1,1) blocks (admm_solver.cpp:144-290)
+// with the inner solvers of local_opt.cpp: Gauss-Newton (squared L2,
+// :20-82) and L-BFGS (Huber, :84-186). One thread owns one observation's
+// 9-dim problem (point copy x_i^j, pose copy y_j^i); every branch of the
+// reference control flow (damping escalation, non-strict accept, step/grad
+// exits, Armijo backtracking, Powell damping, history eviction) is kept.
+//
+// B200 choices: SoA camera-side state read with one coalesced 8 B load per
+// component; the point-side 64 B record gathered from point-major order (the
+// only irregular access of the round lives here, hidden behind FP64 work);
+// the damped normal equations H + lambda*diag = A^T A + D (A = 2x9 projection
+// Jacobian, D diagonal >= rho/2) solved exactly by Woodbury with a 2x2
+// capacitance matrix instead of a dense 9x9 LDLT.
+#pragma once
+
+#include "dbag_common.cuh"
+
+namespace dbag {
+
+constexpr double kDampingInit = 1e-4;  // local_opt.cpp:13
+constexpr double kDampingMax = 1e12;   // local_opt.cpp:14
+
+struct LocalCounters {
+  unsigned n_jac = 0, n_trial = 0, n_acc = 0, n_dir = 0, n_pairs = 0;
+};
+
+__device__ __forceinline__ void flush_counters(const DevState& S, const LocalCounters& c) {
+  // warp-aggregate then one atomic per warp into a striped counter slot
+  unsigned long long v[5] = {c.n_jac, c.n_trial, c.n_acc, c.n_dir, c.n_pairs};
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned long long* slot =
+      S.counters + 8 * ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % kCounterStripes);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    unsigned long long s = warp_sum(v[k]);
+    if (lane == 0 && s) atomicAdd(slot + k, s);
+  }
+}
+
+// Residual of the squared-L2 local problem at v (admm_solver.cpp:187-206):
+// r = [z - pi(v) ; wx (v_x - tx) ; wy (v_y - ty)], objective ||r||^2 summed in
+// row order. Returns false when the projection is infeasible.
+struct GnProblem {
+  double tgt[9];   // x~ (3) and y~ (6): completed-square targets (:152-164)
+  double z0, z1, f, wx, wy, eps;
+};
+
+__device__ __forceinline__ bool gn_residual(const GnProblem& P, const double v[9], Trig& tr,
+                                            double R[9], double w[3], double& e0, double& e1,
+                                            double& obj) {
+  trig_of(v[3], v[4], v[5], tr);
+  rot_of(tr, R);
+  cam_point(R, v, v + 6, w);
+  if (!feasible(w[2], P.eps)) return false;
+  e0 = P.z0 - P.f * w[0] / w[2];
+  e1 = P.z1 - P.f * w[1] / w[2];
+  double s = e0 * e0 + e1 * e1;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const double wk = k < 3 ? P.wx : P.wy;
+    const double rk = wk * (v[k] - P.tgt[k]);
+    s += rk * rk;
+  }
+  obj = s;
+  return true;
+}
+
+// Projection Jacobian A = d pi / d v (2x9) at v, given R and w = Rx + t
+// (geometry.cpp:52-58,141-159): A[:,0:3] = D R, A[:,3+k] = D (dR_k x),
+// A[:,6:9] = D. dR_k x uses the staged products Rz Ry Rx.
+__device__ __forceinline__ void proj_jacobian(const double v[9], const Trig& t, const double R[9],
+                                              const double w[3], double f, double A0[9],
+                                              double A1[9]) {
+  const double inv_z = 1.0 / w[2];
+  const double a = f * inv_z;
+  const double b0 = -f * w[0] * inv_z * inv_z;
+  const double b1 = -f * w[1] * inv_z * inv_z;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    A0[c] = a * R[c] + b0 * R[6 + c];
+    A1[c] = a * R[3 + c] + b1 * R[6 + c];
+  }
+  // q = Rx x, s = Ry q, Rx' = R x (no t)
+  const double q1 = t.ca * v[1] - t.sa * v[2];
+  const double q2 = t.sa * v[1] + t.ca * v[2];
+  const double q0 = v[0];
+  const double s0 = t.cb * q0 + t.sb * q2;
+  const double s2 = -t.sb * q0 + t.cb * q2;
+  // d/dalpha: Rz Ry (0, -q2, q1)
+  const double da0 = t.cg * (t.sb * q1) + t.sg * q2;
+  const double da1 = t.sg * (t.sb * q1) - t.cg * q2;
+  const double da2 = t.cb * q1;
+  // d/dbeta: Rz (s2, 0, -s0)
+  const double db0 = t.cg * s2, db1 = t.sg * s2, db2 = -s0;
+  // d/dgamma: (-(Rx)_1, (Rx)_0, 0)
+  const double rx0 = R[0] * v[0] + R[1] * v[1] + R[2] * v[2];
+  const double rx1 = R[3] * v[0] + R[4] * v[1] + R[5] * v[2];
+  const double dg0 = -rx1, dg1 = rx0;
+  A0[3] = a * da0 + b0 * da2;
+  A1[3] = a * da1 + b1 * da2;
+  A0[4] = a * db0 + b0 * db2;
+  A1[4] = a * db1 + b1 * db2;
+  A0[5] = a * dg0;
+  A1[5] = a * dg1;
+  A0[6] = a;
+  A1[6] = 0.0;
+  A0[7] = 0.0;
+  A1[7] = a;
+  A0[8] = b0;
+  A1[8] = b1;
+}
+
+// gauss_newton (local_opt.cpp:20-82) on the 11-row residual. Returns false if
+// the residual is undefined at the start (the reference throws).
+__device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, double v[9],
+                                         LocalCounters& cnt) {
+  Trig tr;
+  double R[9], w[3], e0, e1, obj;
+  if (!gn_residual(P, v, tr, R, w, e0, e1, obj) || !isfinite(e0) || !isfinite(e1) ||
+      !isfinite(obj))
+    return false;
+  const double wx2 = P.wx * P.wx, wy2 = P.wy * P.wy;
+  for (int it = 0; it < S.inner_max_iters; ++it) {
+    // J = [-A ; diag(w)] at v
+    double A0[9], A1[9];
+    proj_jacobian(v, tr, R, w, P.f, A0, A1);
+    ++cnt.n_jac;
+    double rhs[9], g2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const double wk = k < 3 ? P.wx : P.wy;
+      const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.tgt[k]));
+      rhs[k] = -jtr;                 // -0.5 g
+      const double gk = 2.0 * jtr;   // g = 2 J^T r
+      g2 += gk * gk;
+    }
+    if (sqrt(g2) <= S.grad_tol) return true;  // kGradConverged
+    double lambda = 0.0;
+    for (;;) {
+      // (A^T A + D) delta = rhs, D_k = w_k^2 + lambda*max(H_kk, 1e-12)
+      double iD[9], u[9];
+      double c00 = 1.0, c01 = 0.0, c11 = 1.0, a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const double wk2 = k < 3 ? wx2 : wy2;
+        double Dk = wk2;
+        if (lambda > 0.0) {
+          const double hkk = (A0[k] * A0[k] + A1[k] * A1[k]) + wk2;
+          Dk = wk2 + lambda * fmax(hkk, 1e-12);
+        }
+        iD[k] = __drcp_rn(Dk);
+        u[k] = rhs[k] * iD[k];
+        c00 += A0[k] * A0[k] * iD[k];
+        c01 += A0[k] * A1[k] * iD[k];
+        c11 += A1[k] * A1[k] * iD[k];
+        a0 += A0[k] * u[k];
+        a1 += A1[k] * u[k];
+      }
+      const double det = c00 * c11 - c01 * c01;
+      const double y0 = (c11 * a0 - c01 * a1) / det;
+      const double y1 = (c00 * a1 - c01 * a0) / det;
+      double vt[9], d2 = 0.0;
+      bool fin = true;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const double dk = u[k] - iD[k] * (A0[k] * y0 + A1[k] * y1);
+        fin = fin && isfinite(dk);
+        d2 += dk * dk;
+        vt[k] = v[k] + dk;
+      }
+      if (fin) {
+        Trig trt;
+        double Rt[9], wt[3], et0, et1, objt;
+        ++cnt.n_trial;
+        if (gn_residual(P, vt, trt, Rt, wt, et0, et1, objt) && isfinite(et0) && isfinite(et1) &&
+            isfinite(objt) && objt <= obj) {
+          ++cnt.n_acc;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) v[k] = vt[k];
+#pragma unroll
+          for (int k = 0; k < 9; ++k) R[k] = Rt[k];
+          tr = trt;
+          w[0] = wt[0];
+          w[1] = wt[1];
+          w[2] = wt[2];
+          e0 = et0;
+          e1 = et1;
+          obj = objt;
+          double x2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) x2 += v[k] * v[k];
+          if (sqrt(d2) <= S.step_tol * (1.0 + sqrt(x2))) return true;  // kStepConverged
+          break;
+        }
+      }
+      lambda = lambda == 0.0 ? kDampingInit : lambda * 10.0;
+      if (lambda > kDampingMax) return true;  // kLineSearchFailed / kSingularSystem
+    }
+  }
+  return true;  // kMaxIters
+}
+
+// K1 entry: blocks [begin, begin+count) in block order.
+template <int kLoss>
+__global__ void __launch_bounds__(128) k_local(DevState S, int64_t begin, int64_t count) {
+  const int64_t b = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  LocalCounters cnt;
+  if (b < begin + count) {
+    const int32_t j = S.blk_cam[b];
+    const int32_t i = S.blk_pt[b];
+    const int32_t p = S.blk_pos[b];
+    const double* yb = S.ybar + 8 * (int64_t)j;
+    const double4 xb = S.xbar[i];
+    const PointRec rec = S.prec[p];
+    double v[9], sd[6];
+    v[0] = rec.x0;
+    v[1] = rec.x1;
+    v[2] = rec.x2;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      v[3 + k] = S.cam_soa[(int64_t)k * S.L + b];
+      sd[k] = S.cam_soa[(int64_t)(6 + k) * S.L + b];
+    }
+    bool ok;
+    if (kLoss == 0) {
+      GnProblem P;
+      // completed-square targets x~ = xbar - r/rho, y~ = ybar - s/rho (:152-164)
+      P.tgt[0] = xb.x - rec.r0 / S.rho_x;
+      P.tgt[1] = xb.y - rec.r1 / S.rho_x;
+      P.tgt[2] = xb.z - rec.r2 / S.rho_x;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) P.tgt[3 + k] = yb[k] - sd[k] / S.rho_y;
+      P.z0 = rec.u;
+      P.z1 = rec.v;
+      P.f = yb[6];
+      P.wx = sqrt(0.5 * S.rho_x);  // :183-184
+      P.wy = sqrt(0.5 * S.rho_y);
+      P.eps = S.eps_depth;
+      ok = local_gn(S, P, v, cnt);
+    } else {
+      ok = false;  // Huber path: see dbag_lbfgs.cuh (k_local<1> specialisation)
+    }
+    if (!ok) {
+      atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)b);
+    } else {
+      double* xp = reinterpret_cast<double*>(S.prec + p);
+      xp[0] = v[0];
+      xp[1] = v[1];
+      xp[2] = v[2];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) S.cam_soa[(int64_t)k * S.L + b] = v[3 + k];
+    }
+  }
+  flush_counters(S, cnt);
+}
+
+}  // namespace dbag
