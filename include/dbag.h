@@ -93,7 +93,15 @@ typedef struct {
   int32_t workers;         /* validated >= 1 (reference semantics); unused on GPU */
   int32_t points_per_block, cameras_per_block; /* only (1,1) is built */
   int32_t device;          /* CUDA device ordinal */
+  int32_t numerics;        /* dbag_numerics */
 } dbag_options;
+
+/* EXACT: every operation of the restated reference in the same order (no FMA
+ * contraction, dense pivoted LDLT, sequential reductions, portable sin/cos):
+ * the state trajectory is bit-identical to oracle/ (DESIGN.md §Parity).
+ * FAST: FMA, Woodbury 2x2 solve, hardware sin/cos, tree reductions — the same
+ * algorithm and control flow, different last-ulp rounding. */
+typedef enum { DBAG_NUMERICS_FAST = 0, DBAG_NUMERICS_EXACT = 1 } dbag_numerics;
 
 #define DBAG_MAX_LBFGS_MEMORY 8
 

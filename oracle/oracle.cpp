@@ -51,30 +51,76 @@ Vec3 mat_vec(const Mat3& a, const Vec3& x) {
           a[6] * x[0] + a[7] * x[1] + a[8] * x[2]};
 }
 
+// Portable deterministic sin/cos (<= 1 ulp from glibc; +, -, *, rint only, no
+// FMA): Cody-Waite reduction by pi/2 with a 33+33+53-bit split, Taylor
+// polynomials to x^17 / x^18 on [-pi/4, pi/4], compensated cos. The device's
+// exact-numerics mode evaluates the same algorithm, so oracle and device agree
+// bit for bit; the reference's std::sin/std::cos (geometry.cpp:9-49) are
+// glibc's, whose last-ulp behaviour is unpinned like Eigen's.
+void det_sincos(double x, double* sn, double* cs) {
+  constexpr double kH1 = 1.5707963267341256, kH2 = 6.077100506303966e-11,
+                   kH3 = 2.0222662487959506e-21, kTwoOverPi = 0.6366197723675814;
+  const double k = std::nearbyint(x * kTwoOverPi);
+  const double r = ((x - k * kH1) - k * kH2) - k * kH3;
+  const double z = r * r;
+  double p = 2.8114572543455206e-15;
+  p = p * z + -7.647163731819816e-13;
+  p = p * z + 1.6059043836821613e-10;
+  p = p * z + -2.505210838544172e-08;
+  p = p * z + 2.7557319223985893e-06;
+  p = p * z + -0.0001984126984126984;
+  p = p * z + 0.008333333333333333;
+  p = p * z + -0.16666666666666666;
+  const double s = r + (r * z) * p;
+  double q = -1.5619206968586225e-16;
+  q = q * z + 4.779477332387385e-14;
+  q = q * z + -1.1470745597729725e-11;
+  q = q * z + 2.08767569878681e-09;
+  q = q * z + -2.755731922398589e-07;
+  q = q * z + 2.48015873015873e-05;
+  q = q * z + -0.001388888888888889;
+  q = q * z + 0.041666666666666664;
+  const double hz = 0.5 * z;
+  const double w = 1.0 - hz;
+  const double c = w + (((1.0 - w) - hz) + (z * z) * q);
+  switch (static_cast<long long>(k) & 3) {
+    case 0: *sn = s; *cs = c; break;
+    case 1: *sn = c; *cs = -s; break;
+    case 2: *sn = -s; *cs = -c; break;
+    default: *sn = -c; *cs = s; break;
+  }
+}
+
 namespace {
 // proj/src/geometry.cpp:9-49
 Mat3 rot_x(double a) {
-  const double c = std::cos(a), s = std::sin(a);
+  double c, s;
+  det_sincos(a, &s, &c);
   return {1, 0, 0, 0, c, -s, 0, s, c};
 }
 Mat3 rot_y(double a) {
-  const double c = std::cos(a), s = std::sin(a);
+  double c, s;
+  det_sincos(a, &s, &c);
   return {c, 0, s, 0, 1, 0, -s, 0, c};
 }
 Mat3 rot_z(double a) {
-  const double c = std::cos(a), s = std::sin(a);
+  double c, s;
+  det_sincos(a, &s, &c);
   return {c, -s, 0, s, c, 0, 0, 0, 1};
 }
 Mat3 drot_x(double a) {
-  const double c = std::cos(a), s = std::sin(a);
+  double c, s;
+  det_sincos(a, &s, &c);
   return {0, 0, 0, 0, -s, -c, 0, c, -s};
 }
 Mat3 drot_y(double a) {
-  const double c = std::cos(a), s = std::sin(a);
+  double c, s;
+  det_sincos(a, &s, &c);
   return {-s, 0, c, 0, 0, 0, -c, 0, -s};
 }
 Mat3 drot_z(double a) {
-  const double c = std::cos(a), s = std::sin(a);
+  double c, s;
+  det_sincos(a, &s, &c);
   return {-s, -c, 0, c, -s, 0, 0, 0, 0};
 }
 }  // namespace

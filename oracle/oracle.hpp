@@ -87,6 +87,7 @@ struct Guard {
   double eps_depth = 1e-6;
 };
 
+void det_sincos(double x, double* sn, double* cs);
 Mat3 mat_mul(const Mat3& a, const Mat3& b);
 Vec3 mat_vec(const Mat3& a, const Vec3& x);
 Mat3 rotation_from_euler(double alpha, double beta, double gamma);

@@ -106,6 +106,9 @@ void orc_last_error_info(int* pt, int* cam, double* depth) {
 }
 
 // ---- geometry / losses --------------------------------------------------
+void orc_sincos(int n, const double* x, double* s, double* c) {
+  for (int i = 0; i < n; ++i) det_sincos(x[i], &s[i], &c[i]);
+}
 void orc_rotation_from_euler(double a, double b, double g, double* R) {
   const Mat3 m = rotation_from_euler(a, b, g);
   std::memcpy(R, m.data(), 9 * sizeof(double));

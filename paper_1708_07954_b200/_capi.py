@@ -34,7 +34,8 @@ class Options(C.Structure):
                 ("armijo_c", C.c_double), ("backtrack", C.c_double),
                 ("max_line_search", C.c_int32), ("eps_depth", C.c_double),
                 ("workers", C.c_int32), ("points_per_block", C.c_int32),
-                ("cameras_per_block", C.c_int32), ("device", C.c_int32)]
+                ("cameras_per_block", C.c_int32), ("device", C.c_int32),
+                ("numerics", C.c_int32)]
 
 
 class IterationRecord(C.Structure):

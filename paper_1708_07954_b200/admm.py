@@ -163,6 +163,7 @@ class InnerOptions:
 
 
 SQUARED_L2, HUBER = 0, 1
+FAST, EXACT = 0, 1  # dbag_numerics
 
 
 @dataclass
@@ -200,6 +201,7 @@ class AdmmOptions:
     points_per_block: int = 1
     cameras_per_block: int = 1
     device: int = 0
+    numerics: int = EXACT  # EXACT: bit-identical to the restated reference; FAST: FMA/Woodbury
 
     def _c(self):
         o = _capi.Options()
@@ -213,6 +215,7 @@ class AdmmOptions:
         o.max_line_search, o.eps_depth, o.workers = i.max_line_search, self.eps_depth, self.workers
         o.points_per_block, o.cameras_per_block = self.points_per_block, self.cameras_per_block
         o.device = self.device
+        o.numerics = self.numerics
         return o
 
 

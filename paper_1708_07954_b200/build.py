@@ -11,9 +11,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdbag.so")
-SOURCES = ["dbag_capi.cu", "dbag_scenes.cpp"]
+# (source, extra flags): the exact-numerics TU must not contract a*b+c into
+# FMA — it is a bit-for-bit twin of the oracle's arithmetic.
+SOURCES = [("dbag_capi.cu", []), ("dbag_exact.cu", ["-fmad=false"]), ("dbag_scenes.cpp", [])]
 HEADERS = ["dbag_common.cuh", "dbag_local.cuh", "dbag_lbfgs.cuh", "dbag_consensus.cuh",
-           "dbag_index.cuh"]
+           "dbag_index.cuh", "dbag_exact.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -25,7 +27,7 @@ def nvcc():
 
 
 def _inputs():
-    files = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    files = [os.path.join(CSRC, s) for s, _ in SOURCES] + [os.path.join(CSRC, h) for h in HEADERS]
     files.append(os.path.join(HERE, "..", "include", "dbag.h"))
     files.append(os.path.abspath(__file__))
     return files
@@ -41,15 +43,26 @@ def up_to_date():
 def build(force=False, verbose=False, extra=()):
     if not force and up_to_date():
         return LIB
-    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v" if verbose else "-O3", *extra,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+    objdir = os.path.join(HERE, "_obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for src, flags in SOURCES:
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
+               "-Xptxas", "-v" if verbose else "-O3", *flags, *extra, "-c",
+               os.path.join(CSRC, src), "-o", obj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError(f"nvcc failed on {src}")
+        if verbose:
+            sys.stderr.write(res.stderr)
+        objs.append(obj)
+    cmd = [nvcc(), *ARCH, "-shared", *objs, "-o", LIB + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libdbag.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc link failed for libdbag.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

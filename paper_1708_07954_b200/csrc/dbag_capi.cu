@@ -14,6 +14,7 @@
 #include "../../include/dbag.h"
 #include "dbag_common.cuh"
 #include "dbag_consensus.cuh"
+#include "dbag_exact.h"
 #include "dbag_index.cuh"
 #include "dbag_local.cuh"
 #include "dbag_lbfgs.cuh"
@@ -114,7 +115,52 @@ struct dbag_solver {
     if (stream) cudaStreamDestroy(stream);
   }
 
+  bool exact() const { return opts.numerics == DBAG_NUMERICS_EXACT; }
+
+  void launch_camera(int mode) {
+    if (exact()) {
+      CK(exact::launch_camera(S, mode, stream));
+      return;
+    }
+    if (mode == kModeConsensus)
+      k_camera<kModeConsensus><<<S.M, kCamThreads, 0, stream>>>(S);
+    else if (mode == kModeDual)
+      k_camera<kModeDual><<<S.M, kCamThreads, 0, stream>>>(S);
+    else
+      k_camera<kModeConsensus | kModeDual><<<S.M, kCamThreads, 0, stream>>>(S);
+    CK_LAUNCH();
+  }
+
+  void launch_point(int mode, bool metric) {
+    if (exact()) {
+      CK(exact::launch_point(S, mode, metric, n_pt_parts, stream));
+      return;
+    }
+    if (mode == kModeConsensus)
+      k_point<kModeConsensus, false><<<n_pt_parts, kPtThreads, 0, stream>>>(S);
+    else if (mode == kModeDual)
+      k_point<kModeDual, false><<<n_pt_parts, kPtThreads, 0, stream>>>(S);
+    else if (metric)
+      k_point<kModeConsensus | kModeDual, true><<<n_pt_parts, kPtThreads, 0, stream>>>(S);
+    else
+      k_point<kModeConsensus | kModeDual, false><<<n_pt_parts, kPtThreads, 0, stream>>>(S);
+    CK_LAUNCH();
+  }
+
+  void launch_camR_all() {
+    if (exact()) {
+      CK(exact::launch_camR_all(S, stream));
+    } else {
+      k_camR_all<<<grid_for(S.M, 128), 128, 0, stream>>>(S);
+      CK_LAUNCH();
+    }
+  }
+
   void launch_local(int64_t begin, int64_t count) {
+    if (exact()) {
+      CK(exact::launch_local(S, begin, count, stream));
+      return;
+    }
     const unsigned g = grid_for(count, 128);
     if (opts.loss == DBAG_LOSS_SQUARED_L2)
       k_local<0><<<g, 128, 0, stream>>>(S, begin, count);
@@ -141,11 +187,9 @@ struct dbag_solver {
     CK(cudaEventRecord(e[0], stream));
     launch_local(0, S.L);
     CK(cudaEventRecord(e[1], stream));
-    k_camera<kModeConsensus | kModeDual><<<S.M, kCamThreads, 0, stream>>>(S);
-    CK_LAUNCH();
+    launch_camera(kModeConsensus | kModeDual);
     CK(cudaEventRecord(e[2], stream));
-    k_point<kModeConsensus | kModeDual, true><<<n_pt_parts, kPtThreads, 0, stream>>>(S);
-    CK_LAUNCH();
+    launch_point(kModeConsensus | kModeDual, true);
     CK(cudaEventRecord(e[3], stream));
     if (with_ref) {
       k_mse<<<n_mse_parts, 256, 0, stream>>>(S);
@@ -214,8 +258,7 @@ struct dbag_solver {
 
   double reproj_sum(int power, bool throw_depth, const std::vector<double>* host_pose = nullptr) {
     CK(cudaMemsetAsync(S.err_obs, 0xff, sizeof(int64_t), stream));
-    k_camR_all<<<grid_for(S.M, 128), 128, 0, stream>>>(S);
-    CK_LAUNCH();
+    launch_camR_all();
     const int parts = std::max(1, std::min(n_pt_parts, 4096));
     if (power == 1)
       k_reproj_blocks<1><<<parts, 256, 0, stream>>>(S);
@@ -295,6 +338,7 @@ void dbag_options_default(dbag_options* o) {
   o->points_per_block = 1;
   o->cameras_per_block = 1;
   o->device = 0;
+  o->numerics = DBAG_NUMERICS_EXACT;
 }
 
 int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const dbag_options* opts,
@@ -518,6 +562,8 @@ int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const d
     }
     // init must be feasible (admm_solver.cpp:116 -> problem.cpp:140-157)
     h->reproj_sum(1, true);
+    if (o.numerics != DBAG_NUMERICS_FAST && o.numerics != DBAG_NUMERICS_EXACT)
+      raise(DBAG_ERR_VALIDATION, "numerics must be FAST (0) or EXACT (1)");
     if (o.points_per_block < 1 || o.cameras_per_block < 1)
       raise(DBAG_ERR_VALIDATION, "block sizes must be >= 1");
     if (o.points_per_block != 1 || o.cameras_per_block != 1)
@@ -557,10 +603,8 @@ int dbag_local_update_all(dbag_solver* h) {
 int dbag_consensus_update(dbag_solver* h) {
   return guarded([&] {
     CK(cudaSetDevice(h->device));
-    k_camera<kModeConsensus><<<h->S.M, kCamThreads, 0, h->stream>>>(h->S);
-    CK_LAUNCH();
-    k_point<kModeConsensus, false><<<h->n_pt_parts, kPtThreads, 0, h->stream>>>(h->S);
-    CK_LAUNCH();
+    h->launch_camera(kModeConsensus);
+    h->launch_point(kModeConsensus, false);
     h->sync();
   });
 }
@@ -568,10 +612,8 @@ int dbag_consensus_update(dbag_solver* h) {
 int dbag_dual_update(dbag_solver* h) {
   return guarded([&] {
     CK(cudaSetDevice(h->device));
-    k_camera<kModeDual><<<h->S.M, kCamThreads, 0, h->stream>>>(h->S);
-    CK_LAUNCH();
-    k_point<kModeDual, false><<<h->n_pt_parts, kPtThreads, 0, h->stream>>>(h->S);
-    CK_LAUNCH();
+    h->launch_camera(kModeDual);
+    h->launch_point(kModeDual, false);
     h->sync();
   });
 }

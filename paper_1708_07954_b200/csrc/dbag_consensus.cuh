@@ -18,41 +18,6 @@ constexpr int kModeConsensus = 1, kModeDual = 2;
 constexpr int kCamThreads = 256;
 constexpr int kPtThreads = 256;
 
-template <int NT, int K>
-__device__ __forceinline__ void block_sum(double (&v)[K], double* smem /*[NT/32][K]*/) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) smem[wid * K + k] = v[k];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double s = smem[k];
-      for (int w = 1; w < NT / 32; ++w) s += smem[w * K + k];
-      v[k] = s;
-    }
-  }
-  __syncthreads();
-}
-
-template <int NT>
-__device__ __forceinline__ double block_max(double v, double* smem) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = warp_max(v);
-  if (lane == 0) smem[wid] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = smem[0];
-    for (int w = 1; w < NT / 32; ++w) s = fmax(s, smem[w]);
-    v = s;
-  }
-  __syncthreads();
-  return v;
-}
-
 __device__ __forceinline__ void write_camR(const DevState& S, int j, const double* pose, double f) {
   Trig t;
   trig_of(pose[0], pose[1], pose[2], t);

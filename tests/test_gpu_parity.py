@@ -4,9 +4,14 @@ oracle (the restated reference) on the same seeded inputs.
 Bars (BASELINE.json north_star): integer indexing bit-exact; per-round
 objective (mean reprojection error) and primal/dual residuals within 1e-9
 relative; final camera/point parameters within 1e-6 relative, fp64 throughout.
-Residual maxima near convergence are differences of nearly equal numbers, so
-their check carries an absolute floor of 1e-9 * (1 + |x|_inf) where x is
-the state they are differences of.
+
+The reference iteration is chaotic (a last-ulp change grows to 1e-2 in 50
+rounds; tests/test_sensitivity.py measures it on the oracle itself), so those
+bars are met by the EXACT numerics mode, whose state trajectory is
+BIT-IDENTICAL to the oracle's (the tests below assert equality, a stronger
+bar). Its reported sums (mean reprojection error, MSE) use a tree order and
+agree to 1e-12. The FAST mode (FMA, Woodbury solve, hardware sin/cos) is
+checked one round at a time from identical states.
 """
 import numpy as np
 import pytest
@@ -26,7 +31,7 @@ def P():
     return P
 
 
-def pair(O, P, problem_arrays, init, **kw):
+def pair(O, P, problem_arrays, init, numerics=1, **kw):
     """Oracle solver and GPU solver on identical inputs."""
     cam_pose, cam_f, points, cam, pt, uv = problem_arrays
     ip, ix = init
@@ -39,7 +44,7 @@ def pair(O, P, problem_arrays, init, **kw):
     gprob = P.Problem.create(cam_pose, cam_f, points, cam, pt, uv)
     opts = P.AdmmOptions(misfit_loss=P.LossKind(loss, kw.get("huber_delta", 1.0)),
                          rho_x=kw.get("rho_x", 1.0), rho_y=kw.get("rho_y", 1.0),
-                         max_iters=kw.get("max_iters", 1600))
+                         max_iters=kw.get("max_iters", 1600), numerics=numerics)
     opts.inner.max_iters = inner_iters
     gsol = P.AdmmSolver(gprob, P.ParamState(ip, cam_f, ix), opts)
     return oprob, osol, gsol
@@ -62,6 +67,8 @@ def config_arrays(P, config, seed=0, scale=1.0):
 
 
 def rel_close(a, b, rel, floor=0.0):
+    if a == b:  # also inf == inf (infeasible consensus on both sides)
+        return True
     return abs(a - b) <= rel * max(abs(a), abs(b)) + floor
 
 
@@ -77,6 +84,28 @@ def assert_trajectory(otrace, gtrace, scale_x, scale_y, rel=REL_METRIC):
             worst[k] = max(worst.get(k, 0.0), d)
             assert rel_close(o[k], g[k], rel, floor), (k, o["iter"], o[k], g[k])
     return worst
+
+
+def assert_exact_trajectory(otrace, gtrace):
+    """EXACT mode: residual maxima bitwise (max of identical values), sums 1e-12."""
+    assert len(otrace) == len(gtrace)
+    for o, g in zip(otrace, gtrace):
+        assert o["iter"] == g["iter"] and o["comm_floats"] == g["comm_floats"]
+        assert o["max_primal_x"] == g["max_primal_x"], (o["iter"], o["max_primal_x"], g["max_primal_x"])
+        assert o["max_primal_y"] == g["max_primal_y"], (o["iter"], o["max_primal_y"], g["max_primal_y"])
+        for k in ("mean_reproj_err", "camera_mse", "point_mse"):
+            if k in o and not (np.isnan(o[k]) and np.isnan(g[k])):
+                assert rel_close(o[k], g[k], 1e-12, 1e-300), (k, o["iter"], o[k], g[k])
+
+
+def assert_state_identical(osol, g):
+    opose, _, opts = osol.consensus()
+    gc = g.consensus()
+    assert np.array_equal(opose, gc.cam_pose) and np.array_equal(opts, gc.points)
+    lp, lc, r, s = osol.copies()
+    st = g.state()
+    assert np.array_equal(lp, st.local_points) and np.array_equal(lc, st.local_cameras)
+    assert np.array_equal(r, st.dual_r) and np.array_equal(s, st.dual_s)
 
 
 def assert_params(oc, gc, rel=REL_PARAM):
@@ -253,6 +282,7 @@ def test_local_update_matches_oracle_and_never_increases(O, P):
             after = g.block_objective(b)
             assert after <= before + 1e-12 * abs(before)
             assert rel_close(after, osol.block_objective(b), 1e-9, 1e-12)
+        assert_state_identical(osol, g)
 
 
 def test_dual_sums_vanish(O, P):
@@ -292,13 +322,13 @@ def test_consensus_bit_identical_to_oracle_on_same_copies(O, P):
     opose, _, opts = osol.consensus()
     gc = g.consensus()
     assert np.array_equal(opts, gc.points)
-    assert np.allclose(opose, gc.cam_pose, rtol=1e-14, atol=1e-15)
+    assert np.array_equal(opose, gc.cam_pose)
     g.dual_update()
     osol.dual_update()
     _, _, orr, oss = osol.copies()
     st = g.state()
     assert np.array_equal(orr, st.dual_r)
-    assert np.allclose(oss, st.dual_s, rtol=1e-13, atol=1e-14)
+    assert np.array_equal(oss, st.dual_s)
 
 
 # ---------------------------------------------------------------------------
@@ -306,17 +336,14 @@ def test_consensus_bit_identical_to_oracle_on_same_copies(O, P):
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("seed,sc,sp,loss,rounds", [(93, 0.01, 0.01, 0, 40), (100, 0.05, 0.2, 0, 40),
                                                      (85, 0.05, 0.3, 1, 20)])
-def test_orbit_trajectory_parity(O, P, seed, sc, sp, loss, rounds):
+def test_orbit_trajectory_exact(O, P, seed, sc, sp, loss, rounds):
     arrays, init = orbit_arrays(O, seed, sc, sp)
     oprob, osol, g = pair(O, P, arrays, init, loss=loss, max_iters=rounds)
     ref = P.ParamState(arrays[0], arrays[1], arrays[2])
     ot = osol.run(arrays[0], arrays[2])
     gt = g.run(ref)
-    assert_trajectory(ot, gt, np.abs(arrays[2]).max(), np.abs(arrays[0]).max())
-    for o, gg in zip(ot, gt):
-        assert rel_close(o["camera_mse"], gg["camera_mse"], 1e-9, 1e-18)
-        assert rel_close(o["point_mse"], gg["point_mse"], 1e-9, 1e-18)
-    assert_params(osol.consensus(), g.consensus())
+    assert_exact_trajectory(ot, gt)
+    assert_state_identical(osol, g)
 
 
 def test_golden_fixture_trajectories(O, P):
@@ -329,9 +356,10 @@ def test_golden_fixture_trajectories(O, P):
         arrays, init = orbit_arrays(O, case["seed"], case["sigma_cam"], case["sigma_point"])
         _, _, g = pair(O, P, arrays, init, loss=case["loss"], max_iters=case["rounds"])
         gt = g.run(P.ParamState(arrays[0], arrays[1], arrays[2]))
-        assert_trajectory(case["trace"], gt, np.abs(arrays[2]).max(), np.abs(arrays[0]).max())
+        assert_exact_trajectory(case["trace"], gt)
         fc = g.consensus()
-        assert_params((np.array(case["final_pose"]), None, np.array(case["final_pts"])), fc)
+        assert np.array_equal(np.array(case["final_pose"]), fc.cam_pose)
+        assert np.array_equal(np.array(case["final_pts"]), fc.points)
 
 
 @pytest.mark.parametrize("loss,rounds", [(1, 50), (0, 50)])
@@ -342,9 +370,8 @@ def test_config1_parity(O, P, loss, rounds):
     _, osol, g = pair(O, P, arrays, init, loss=loss, max_iters=rounds)
     ot = osol.run(scene.ground_truth.cam_pose, scene.ground_truth.points)
     gt = g.run(scene.ground_truth)
-    w = assert_trajectory(ot, gt, np.abs(arrays[2]).max(), np.abs(arrays[0]).max())
-    print("config1 loss", loss, "worst rel", w)
-    assert_params(osol.consensus(), g.consensus())
+    assert_exact_trajectory(ot, gt)
+    assert_state_identical(osol, g)
 
 
 @pytest.mark.parametrize("config,scale,rounds,loss", [(2, 0.25, 10, 0), (2, 0.1, 10, 1),
@@ -355,8 +382,36 @@ def test_config_parity_scaled(O, P, config, scale, rounds, loss):
     _, osol, g = pair(O, P, arrays, init, loss=loss, max_iters=rounds)
     ot = osol.run()
     gt = g.run()
-    assert_trajectory(ot, gt, np.abs(arrays[2]).max(), np.abs(arrays[0]).max())
-    assert_params(osol.consensus(), g.consensus())
+    assert_exact_trajectory(ot, gt)
+    assert_state_identical(osol, g)
+
+
+@pytest.mark.parametrize("config,scale,loss", [(1, 1.0, 0), (1, 1.0, 1), (2, 0.1, 0), (2, 0.1, 1),
+                                               (5, 0.002, 0)])
+def test_fast_mode_one_round_from_identical_state(O, P, config, scale, loss):
+    """FAST numerics, one local+consensus+dual round from the oracle's state
+    after 3 rounds: copies agree per observation far inside 1e-6 relative; the
+    round's metrics within 1e-9 relative."""
+    arrays, init, scene = config_arrays(P, config, 2, scale)
+    _, osol, g = pair(O, P, arrays, init, numerics=0, loss=loss, max_iters=100)
+    for _ in range(3):
+        osol.iterate()
+    lp, lc, r, s = osol.copies()
+    opose, _, opts = osol.consensus()
+    g.set_copies(lp, lc, r, s)
+    g.set_consensus(P.ParamState(opose, arrays[1], opts))
+    o1 = osol.iterate()
+    g1 = g.iterate()
+    lp2, lc2, _, _ = osol.copies()
+    st = g.state()
+    scale_p = np.maximum(np.abs(lp2), 1.0)
+    scale_c = np.maximum(np.abs(lc2), 1.0)
+    dp = np.abs(st.local_points - lp2) / scale_p
+    dc = np.abs(st.local_cameras - lc2) / scale_c
+    print("fast one-round: median/max rel point", np.median(dp), dp.max(), "cam", np.median(dc), dc.max())
+    assert np.median(dp) < 1e-12 and np.median(dc) < 1e-12
+    assert dp.max() < 1e-6 and dc.max() < 1e-6
+    assert rel_close(o1["mean_reproj_err"], g1["mean_reproj_err"], 1e-9)
 
 
 # ---------------------------------------------------------------------------
