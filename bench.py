@@ -40,7 +40,8 @@ CONFIG_NAMES = {1: "config1-tiny-ring", 2: "config2-medium-hemisphere", 3: "conf
 
 # Algorithmic-work model (Woodbury variant):
 # transcendentals, div and sqrt count as one flop each.
-GN_FLOPS = {"jac": 312, "trial": 190, "acc": 38}
+GN_FLOPS = {"jac": 312, "trial": 190, "acc": 38}          # FAST: Woodbury 2x2 solve
+GN_FLOPS_EXACT = {"jac": 312, "trial": 520, "acc": 38}    # EXACT: dense pivoted 9x9 LDLT
 LBFGS_FLOPS = {"grad": 175, "value": 95, "dir": 18, "dir_pair": 72, "pair": 100}
 # Compulsory HBM bytes per observation per kernel (DESIGN.md §HBM layout).
 BYTES_PER_OBS = {"local": 276.0, "camera": 144.0, "point": 92.0}
@@ -109,10 +110,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def flops_of(stats, loss):
+def flops_of(stats, loss, numerics="exact"):
     if loss == "l2":
-        return (GN_FLOPS["jac"] * stats["n_jacobian"] + GN_FLOPS["trial"] * stats["n_trial"] +
-                GN_FLOPS["acc"] * stats["n_accept"])
+        c = GN_FLOPS_EXACT if numerics == "exact" else GN_FLOPS
+        return (c["jac"] * stats["n_jacobian"] + c["trial"] * stats["n_trial"] +
+                c["acc"] * stats["n_accept"])
     return (LBFGS_FLOPS["grad"] * stats["n_jacobian"] + LBFGS_FLOPS["value"] * stats["n_trial"] +
             LBFGS_FLOPS["dir"] * stats["n_direction"] +
             LBFGS_FLOPS["dir_pair"] * stats["n_pairs_used"] + LBFGS_FLOPS["pair"] * stats["n_accept"])
@@ -199,6 +201,7 @@ def config_block(args, scene):
     return {"workload": CONFIG_NAMES[args.config], "config_id": args.config,
             "cameras": int(p.num_cameras), "points": int(p.num_points),
             "observations": int(p.num_observations), "loss": args.loss,
+            "numerics": args.numerics,
             "rounds_per_solve": args.steps, "seed": args.seed,
             "l2_flush": "not needed: per-round state > 126 MB L2",
             "parallelism": f"camera-sharded x{args.gpus}" if args.gpus > 1 else "single-gpu"}
@@ -218,8 +221,10 @@ def our_arm(args, rank, world, local_rank):
     L = p.num_observations
     loss = P.LossKind.huber(1.0) if args.loss == "huber" else P.LossKind.squared_l2()
 
+    numerics = P.admm.EXACT if args.numerics == "exact" else P.admm.FAST
+
     def opts(rounds):
-        return P.AdmmOptions(misfit_loss=loss, max_iters=rounds, device=dev)
+        return P.AdmmOptions(misfit_loss=loss, max_iters=rounds, device=dev, numerics=numerics)
 
     # ---------------- e2e through the C-ABI from pinned host buffers
     def pinned(a):
@@ -290,7 +295,7 @@ def our_arm(args, rank, world, local_rank):
         kernels[name] = {"ms": ms, "share": stats[key] / max(ms_total, 1e-9),
                          "gbs": byts / (ms / 1e3) / 1e9,
                          "frac_hbm": (byts / (ms / 1e3) / 1e9) / hbm_peak if hbm_peak else None}
-    fl = flops_of(stats, args.loss) / args.steps
+    fl = flops_of(stats, args.loss, args.numerics) / args.steps
     kernels["local"]["tflops"] = fl / (kernels["local"]["ms"] / 1e3) / 1e12
     kernels["local"]["frac_fp64"] = kernels["local"]["tflops"] / fp64_peak
     kernels["local"]["flops_per_obs"] = fl / L
@@ -354,6 +359,8 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--loss", choices=["l2", "huber"], default="l2")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--numerics", choices=["exact", "fast"], default="exact",
+                    help="exact: bit-identical to the restated reference; fast: FMA/Woodbury")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
     args = ap.parse_args()

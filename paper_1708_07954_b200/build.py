@@ -64,7 +64,24 @@ def build(force=False, verbose=False, extra=()):
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed for libdbag.so")
     os.replace(LIB + ".tmp", LIB)
+    build_tools()
     return LIB
+
+
+TOOL_SRC = os.path.join(HERE, "..", "tools", "dbag_solve.cpp")
+TOOL_BIN = os.path.join(HERE, "dbag_solve")
+
+
+def build_tools():
+    """C++ host driver over include/dbag.hpp, linked against the in-tree lib."""
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-O2", "-std=c++17", "-I", os.path.join(HERE, "..", "include"), TOOL_SRC,
+           "-o", TOOL_BIN, "-L", HERE, "-ldbag", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("g++ failed building tools/dbag_solve.cpp against dbag.hpp")
+    return TOOL_BIN
 
 
 if __name__ == "__main__":

@@ -93,3 +93,13 @@ def test_scene_camera_poses_look_at_points():
     # R(2,0) away from the Euler gimbal lock
     b = s.ground_truth.cam_pose[:, 1]
     assert np.all(np.abs(np.sin(b)) < 0.99)
+
+
+def test_cpp_dropin_header_builds():
+    """include/dbag.hpp (reference class names over the C-ABI) compiles and links:
+    tools/dbag_solve.cpp is built against it by build.py."""
+    from paper_1708_07954_b200 import build as b
+    path = b.build_tools()
+    assert os.path.exists(path)
+    out = subprocess.run(["nm", "-D", "--undefined-only", path], capture_output=True, text=True)
+    assert "dbag_create" in out.stdout and "dbag_run" in out.stdout

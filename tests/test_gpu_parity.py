@@ -448,3 +448,27 @@ def test_full_config2_properties(P):
     assert a.mean_reprojection_error() == pytest.approx(ta[-1]["mean_reproj_err"], rel=1e-12)
     # objective decreases from the perturbed init
     assert ta[-1]["mean_reproj_err"] < ta[0]["mean_reproj_err"]
+
+
+def test_cpp_dropin_driver_matches_oracle(O, P):
+    """The C++ host driver (tools/dbag_solve.cpp over include/dbag.hpp) prints the
+    reference metrics CSV; its EXACT trajectory equals the oracle's."""
+    import os
+    import subprocess
+    from paper_1708_07954_b200 import build as b
+    exe = b.TOOL_BIN if os.path.exists(b.TOOL_BIN) else b.build_tools()
+    out = subprocess.run([exe, "1", "10", "huber", "exact"], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    lines = out.stdout.strip().splitlines()
+    assert lines[0] == ("iter,mean_reproj_err,max_primal_x,max_primal_y,camera_mse,point_mse,"
+                        "wall_ms,comm_floats")
+    arrays, init, scene = config_arrays(P, 1, 0)
+    _, osol, _ = pair(O, P, arrays, init, loss=1, max_iters=10)
+    ot = osol.run(scene.ground_truth.cam_pose, scene.ground_truth.points)
+    for line, o in zip(lines[1:], ot):
+        f = line.split(",")
+        assert int(f[0]) == o["iter"]
+        assert float(f[2]) == o["max_primal_x"] and float(f[3]) == o["max_primal_y"]
+        assert rel_close(float(f[1]), o["mean_reproj_err"], 1e-12)
+        assert int(f[7]) == o["comm_floats"]

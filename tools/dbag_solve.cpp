@@ -1,0 +1,62 @@
+// dbag_solve — C++ host driver over the drop-in header (include/dbag.hpp):
+// what `dba solve --solver admm` (tools/dba_main.cpp:231-259) does, on the B200.
+// Generates a BASELINE config scene, runs run_admm, prints the trace in the
+// reference's metrics CSV schema (metrics_csv.hpp:11-12).
+//   dbag_solve <config 1..5> <rounds> [l2|huber] [exact|fast] [scale]
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "dbag.hpp"
+
+int main(int argc, char** argv) {
+  const int config = argc > 1 ? std::atoi(argv[1]) : 1;
+  const int rounds = argc > 2 ? std::atoi(argv[2]) : 50;
+  const bool huber = argc > 3 && std::strcmp(argv[3], "huber") == 0;
+  const bool fast = argc > 4 && std::strcmp(argv[4], "fast") == 0;
+  const double scale = argc > 5 ? std::atof(argv[5]) : 1.0;
+  dbag_scene* sc = nullptr;
+  dbag_scene_info info{};
+  if (dbag_scene_generate(config, 0, scale, &sc, &info) != DBAG_OK) {
+    std::fprintf(stderr, "scene generation failed\n");
+    return 3;
+  }
+  const int m = info.num_cameras, n = info.num_points;
+  const int64_t l = info.num_obs;
+  dba::gpu::Problem problem;
+  problem.obs_cam.resize(l);
+  problem.obs_pt.resize(l);
+  problem.obs_uv.resize(2 * l);
+  problem.nominal.cam_pose.resize(6 * m);
+  problem.nominal.cam_f.resize(m);
+  problem.nominal.points.resize(3 * n);
+  dba::gpu::ParamState init;
+  init.cam_pose.resize(6 * m);
+  init.points.resize(3 * n);
+  dbag_scene_fetch(sc, problem.obs_cam.data(), problem.obs_pt.data(), problem.obs_uv.data(),
+                   problem.nominal.cam_pose.data(), problem.nominal.cam_f.data(),
+                   problem.nominal.points.data(), init.cam_pose.data(), init.points.data());
+  dbag_scene_destroy(sc);
+  init.cam_f = problem.nominal.cam_f;
+  dba::gpu::AdmmOptions opts;
+  opts.max_iters = rounds;
+  opts.misfit_loss = huber ? dba::gpu::LossKind::huber(1.0) : dba::gpu::LossKind::squared_l2();
+  opts.numerics = fast ? DBAG_NUMERICS_FAST : DBAG_NUMERICS_EXACT;
+  try {
+    const dba::gpu::ParamState truth = problem.nominal_state();
+    const dba::gpu::AdmmResult res = dba::gpu::run_admm(problem, init, opts, {}, &truth);
+    std::printf("iter,mean_reproj_err,max_primal_x,max_primal_y,camera_mse,point_mse,wall_ms,comm_floats\n");
+    for (const auto& r : res.trace)
+      std::printf("%d,%.17g,%.17g,%.17g,%.17g,%.17g,%.6g,%lld\n", r.iter, r.mean_reproj_err,
+                  r.max_primal_x, r.max_primal_y, r.camera_mse, r.point_mse, r.wall_ms,
+                  static_cast<long long>(r.comm_floats));
+  } catch (const dba::gpu::ValidationError& e) {
+    std::fprintf(stderr, "data error: %s\n", e.what());
+    return 3;  // dba_main.cpp exit-code convention (:559-568)
+  } catch (const dba::gpu::Error& e) {
+    std::fprintf(stderr, "solver error: %s\n", e.what());
+    return 4;
+  }
+  return 0;
+}
