@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdbag.so")
+LIB_PATH = os.environ.get("DBAG_LIB") or os.path.join(HERE, "libdbag.so")
 
 DPTR = C.POINTER(C.c_double)
 I32P = C.POINTER(C.c_int32)

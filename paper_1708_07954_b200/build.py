@@ -64,7 +64,8 @@ def build(force=False, verbose=False, extra=()):
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed for libdbag.so")
     os.replace(LIB + ".tmp", LIB)
-    build_tools()
+    if os.path.dirname(LIB) == HERE:
+        build_tools()
     return LIB
 
 

@@ -202,9 +202,13 @@ __device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, 
   return true;  // kMaxIters
 }
 
+#ifndef DBAG_K1_MINB
+#define DBAG_K1_MINB 4  // 128 regs: 16 warps/SM beat spill-free 8 warps (84 -> 67 ms, config 5)
+#endif
+
 // K1 entry: blocks [begin, begin+count) in block order.
 template <int kLoss>
-__global__ void __launch_bounds__(128) k_local(DevState S, int64_t begin, int64_t count) {
+__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local(DevState S, int64_t begin, int64_t count) {
   const int64_t b = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   LocalCounters cnt;
   if (b < begin + count) {

@@ -1,0 +1,31 @@
+"""Build libdbag.so variants with different -D tuning macros into
+paper_1708_07954_b200/_variants/<name>.so (A/B timing via DBAG_LIB=...)."""
+import os
+import shutil
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1708_07954_b200 import build as b  # noqa: E402
+
+VARIANTS = {
+    "base": [],
+    "fast_minb3": ["-DDBAG_K1_MINB=3"],
+    "fast_minb4": ["-DDBAG_K1_MINB=4"],
+    "exact_minb3": ["-DDBAG_K1E_MINB=3"],
+}
+
+
+def main(names):
+    out = os.path.join(b.HERE, "_variants")
+    os.makedirs(out, exist_ok=True)
+    saved = b.LIB
+    for n in names or VARIANTS:
+        b.LIB = os.path.join(out, n + ".so")
+        b.build(force=True, extra=VARIANTS[n])
+        print("built", b.LIB)
+    b.LIB = saved
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
