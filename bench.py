@@ -204,7 +204,8 @@ def config_block(args, scene):
             "numerics": args.numerics,
             "rounds_per_solve": args.steps, "seed": args.seed,
             "l2_flush": "not needed: per-round state > 126 MB L2",
-            "parallelism": f"camera-sharded x{args.gpus}" if args.gpus > 1 else "single-gpu"}
+            "parallelism": (f"camera-sharded x{args.gpus}, boundary copies all-gathered over NCCL"
+                            if args.gpus > 1 else "single-gpu")}
 
 
 def our_arm(args, rank, world, local_rank):
@@ -235,16 +236,33 @@ def our_arm(args, rank, world, local_rank):
                    pinned(p.cam_f), pinned(p.points))
     hinit = P.ParamState(pinned(scene.init.cam_pose), pinned(scene.init.cam_f),
                          pinned(scene.init.points))
+
+    def make(prob, init, o):
+        """Single-GPU solver, or this rank's camera shard with the NCCL transport."""
+        if world == 1:
+            return P.AdmmSolver(prob, init, o)
+        s = P.AdmmSolver.sharded(prob, init, o, rank, world)
+        obj = [P.admm.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        s.attach_nccl(obj[0])
+        return s
+
     # warm the context/module once (untimed)
-    w = P.AdmmSolver(hp, hinit, opts(1))
+    w = make(hp, hinit, opts(1))
     w.run()
     w.close()
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
-    s_e2e = P.AdmmSolver(hp, hinit, opts(args.steps))
+    s_e2e = make(hp, hinit, opts(args.steps))
     trace = s_e2e.run()
     final = s_e2e.consensus()
     t_e2e = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([t_e2e], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(t.item())
     s_e2e.close()
     h2d = (p.obs_cam.nbytes + p.obs_pt.nbytes + p.obs_uv.nbytes + p.cam_pose.nbytes +
            p.cam_f.nbytes + p.points.nbytes + scene.init.cam_pose.nbytes +
@@ -254,7 +272,7 @@ def our_arm(args, rank, world, local_rank):
     e2e_value = L * args.steps / t_e2e
 
     # ---------------- device-timed rounds, inputs resident
-    solver = P.AdmmSolver(p, scene.init, opts(10 ** 9))
+    solver = make(p, scene.init, opts(10 ** 9))
     for _ in range(args.warmup):
         solver.enqueue_round()
     solver.synchronize()
@@ -280,17 +298,21 @@ def our_arm(args, rank, world, local_rank):
         ms_total = float(t.item())
     stats = solver.round_stats()
     last = solver.iterate()  # one more round with the metrics read back (untimed)
-    value = L * world * args.steps / (ms_total / 1e3)
+    value = L * args.steps / (ms_total / 1e3)  # whole job: every rank's share of one scene
 
     # ---------------- roofline
     peaks = measured_peaks()
     fp64_peak = P.admm.measure_fp64_peak(dev)
     hbm_peak = peaks.get("hbm_gbs")
     kernels = {}
-    ncam, npt = p.num_cameras, p.num_points
+    # per-rank work (a shard's kernels see its own observations/points/cameras)
+    ncam, npt, Lr = p.num_cameras, p.num_points, L
+    if world > 1:
+        inf_ = solver.plan["info"]
+        ncam, npt, Lr = inf_["cam_end"] - inf_["cam_begin"], inf_["local_points"], inf_["local_obs"]
     for name, key in (("local", "ms_local"), ("camera", "ms_camera"), ("point", "ms_point")):
         ms = stats[key] / args.steps
-        byts = BYTES_PER_OBS[name] * L + BYTES_PER_POINT.get(name, 0) * npt + \
+        byts = BYTES_PER_OBS[name] * Lr + BYTES_PER_POINT.get(name, 0) * npt + \
             BYTES_PER_CAMERA.get(name, 0) * ncam
         kernels[name] = {"ms": ms, "share": stats[key] / max(ms_total, 1e-9),
                          "gbs": byts / (ms / 1e3) / 1e9,
@@ -298,7 +320,7 @@ def our_arm(args, rank, world, local_rank):
     fl = flops_of(stats, args.loss, args.numerics) / args.steps
     kernels["local"]["tflops"] = fl / (kernels["local"]["ms"] / 1e3) / 1e12
     kernels["local"]["frac_fp64"] = kernels["local"]["tflops"] / fp64_peak
-    kernels["local"]["flops_per_obs"] = fl / L
+    kernels["local"]["flops_per_obs"] = fl / Lr
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     if dom == "local":
         roof = {"kernel": "k_local (K1 local solve)", "bound": "fp64",
@@ -338,7 +360,8 @@ def our_arm(args, rank, world, local_rank):
                     "scope": f"dbag_create (H2D + device index build) + {args.steps} rounds "
                              f"(record D2H each) + consensus D2H, wall clock"},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu,
-            "clocks": clocks.summary(), "gpu_launches": 4 * args.steps,
+            "clocks": clocks.summary(),
+            "gpu_launches": (6 if world > 1 else 4) * args.steps,
             "counters": {k: stats[k] for k in ("n_jacobian", "n_trial", "n_accept",
                                                "n_direction", "n_pairs_used")},
             "last_round": {k: last[k] for k in ("iter", "mean_reproj_err", "max_primal_x",

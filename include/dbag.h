@@ -200,6 +200,57 @@ int dbag_reset_stats(dbag_solver* h);
  * roofline denominator, which MEASURED_PEAKS.json does not carry. */
 int dbag_measure_fp64_peak(int32_t device, double* tflops);
 
+/* ---- multi-GPU ---------------------------------------------
+ * Cameras are split into contiguous ranges balanced on observation counts;
+ * rank r owns every observation of its cameras. Boundary points (cameras on
+ * several ranks) exchange their copies' raw (x, r) through one all-gather per
+ * round, so every holder recomputes the reference's sequential consensus sum:
+ * the EXACT trajectory is bit-identical for any number of ranks. Host-only
+ * plan functions below need no GPU (tested with gloo on CPU). */
+typedef struct {
+  int32_t rank, world;
+  int32_t cam_begin, cam_end;   /* this rank's camera range */
+  int64_t local_obs;
+  int32_t local_points;
+  int32_t boundary_points;      /* global */
+  int64_t boundary_copies;      /* global */
+  int64_t send_count, max_send; /* this rank's boundary copies; all-gather slot size */
+  int64_t comm_floats;          /* reference communication_cost (global) */
+} dbag_shard_info;
+typedef struct dbag_shard_plan dbag_shard_plan;
+int dbag_partition_cameras(int32_t m, const int64_t* obs_per_camera, int32_t world,
+                           int32_t* cam_lo /*[world+1]*/);
+int dbag_shard_plan_create(const dbag_problem_view* full, int32_t rank, int32_t world,
+                           dbag_shard_plan** out, dbag_shard_info* info);
+void dbag_shard_plan_get_info(const dbag_shard_plan* s, dbag_shard_info* info);
+/* Any pointer may be NULL. Sizes: cam_lo [world+1]; local_obs [local_obs];
+ * local_points, bp_of_local, owner_of_local [local_points]; gb_off
+ * [boundary_points+1]; gmap [boundary_copies] (recv slot of each global boundary
+ * copy); send_obs_local [send_count] (local observation index of each send slot). */
+int dbag_shard_plan_arrays(const dbag_shard_plan* s, int32_t* cam_lo, int64_t* local_obs,
+                           int32_t* local_points, int32_t* bp_of_local, int8_t* owner_of_local,
+                           int64_t* gb_off, int64_t* gmap, int64_t* send_obs_local);
+void dbag_shard_plan_destroy(dbag_shard_plan* s);
+
+/* A solver for shard `rank` of `world` over the FULL problem/init (every rank
+ * passes the same arrays). Queries return this rank's entries (global ids). */
+int dbag_create_sharded(const dbag_problem_view* full, const dbag_param_view* init,
+                        const dbag_options* opts, int32_t rank, int32_t world,
+                        dbag_solver** out);
+/* NCCL transport: rank 0 makes the id, the launcher broadcasts it, every rank
+ * attaches; iterate/run/enqueue_round then exchange with ncclAllGather. */
+int dbag_nccl_unique_id(uint8_t id[128]);
+int dbag_attach_nccl(dbag_solver* h, const uint8_t id[128]);
+/* External transport (tests, single-device emulation of several ranks): run a
+ * round in phases and copy buffers between handles in between:
+ *   phase 0: local solve + camera consensus/dual + pack boundary copies
+ *   exchange_copy(dst, src, 0) for every (dst, src) pair
+ *   phase 1: point consensus/dual/metric + partial metrics
+ *   exchange_copy(dst, src, 1) for every pair
+ *   phase 2: combine -> *out (only for phase 2; may be NULL otherwise). */
+int dbag_round_phase(dbag_solver* h, int32_t phase, dbag_iteration_record* out);
+int dbag_exchange_copy(dbag_solver* dst, dbag_solver* src, int32_t which);
+
 /* Synthetic scenes of BASELINE.json configs 1-5 (host C++, deterministic in
  * seed). Two-phase: size query, then fill. scale in (0,1]
  * shrinks points/cameras proportionally for bounded samples. */

@@ -66,7 +66,19 @@ class SceneInfo(C.Structure):
                 ("sigma_init", C.c_double)]
 
 
+class ShardInfo(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("cam_begin", C.c_int32),
+                ("cam_end", C.c_int32), ("local_obs", C.c_int64), ("local_points", C.c_int32),
+                ("boundary_points", C.c_int32), ("boundary_copies", C.c_int64),
+                ("send_count", C.c_int64), ("max_send", C.c_int64), ("comm_floats", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 H = C.c_void_p
+I8P = C.POINTER(C.c_int8)
+U8P = C.POINTER(C.c_uint8)
 
 # name -> (restype, argtypes); every symbol declared in include/dbag.h
 SIGNATURES = {
@@ -106,6 +118,18 @@ SIGNATURES = {
     "dbag_get_round_stats": (C.c_int, [H, C.POINTER(RoundStats)]),
     "dbag_reset_stats": (C.c_int, [H]),
     "dbag_measure_fp64_peak": (C.c_int, [C.c_int32, DPTR]),
+    "dbag_partition_cameras": (C.c_int, [C.c_int32, I64P, C.c_int32, I32P]),
+    "dbag_shard_plan_create": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int32,
+                                         C.POINTER(H), C.POINTER(ShardInfo)]),
+    "dbag_shard_plan_get_info": (None, [H, C.POINTER(ShardInfo)]),
+    "dbag_shard_plan_arrays": (C.c_int, [H, I32P, I64P, I32P, I32P, I8P, I64P, I64P, I64P]),
+    "dbag_shard_plan_destroy": (None, [H]),
+    "dbag_create_sharded": (C.c_int, [C.POINTER(ProblemView), C.POINTER(ParamView),
+                                      C.POINTER(Options), C.c_int32, C.c_int32, C.POINTER(H)]),
+    "dbag_nccl_unique_id": (C.c_int, [U8P]),
+    "dbag_attach_nccl": (C.c_int, [H, U8P]),
+    "dbag_round_phase": (C.c_int, [H, C.c_int32, C.POINTER(IterationRecord)]),
+    "dbag_exchange_copy": (C.c_int, [H, H, C.c_int32]),
     "dbag_scene_generate": (C.c_int, [C.c_int32, C.c_uint64, C.c_double, C.POINTER(H),
                                       C.POINTER(SceneInfo)]),
     "dbag_scene_fetch": (C.c_int, [H, I32P, I32P, DPTR, DPTR, DPTR, DPTR, DPTR, DPTR]),

@@ -231,19 +231,48 @@ class AdmmState:
 
 
 class AdmmSolver:
-    """dba::AdmmSolver (admm_solver.hpp:75-138) on one B200."""
+    """dba::AdmmSolver (admm_solver.hpp:75-138) on one B200, or one camera
+    shard of a multi-GPU solve (AdmmSolver.sharded)."""
 
-    def __init__(self, problem: Problem, init: ParamState, opts: AdmmOptions | None = None):
+    def __init__(self, problem: Problem, init: ParamState, opts: AdmmOptions | None = None,
+                 rank: int = 0, world: int = 1):
         self._lib = _capi.load()
         self.problem = problem
         self.opts = opts or AdmmOptions()
         self._h = C.c_void_p()
         init = init.copy()
         pv, iv, o = problem._view(), init._view(), self.opts._c()
-        _check(self._lib.dbag_create(C.byref(pv), C.byref(iv), C.byref(o), C.byref(self._h)))
+        self.rank, self.world = rank, world
+        if world == 1:
+            _check(self._lib.dbag_create(C.byref(pv), C.byref(iv), C.byref(o), C.byref(self._h)))
+        else:
+            _check(self._lib.dbag_create_sharded(C.byref(pv), C.byref(iv), C.byref(o), rank, world,
+                                                 C.byref(self._h)))
         self.m, self.n = problem.num_cameras, problem.num_points
         self.l = problem.num_observations
         self._ref_key = None
+        if world > 1:
+            self.plan = shard_plan(problem, rank, world)
+            info = self.plan["info"]
+            self.l = info["local_obs"]  # per-copy state arrays are this shard's
+
+    @classmethod
+    def sharded(cls, problem, init, opts, rank, world):
+        """Shard `rank` of `world` (cameras split on observation counts)."""
+        return cls(problem, init, opts, rank=rank, world=world)
+
+    def attach_nccl(self, unique_id: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(self._lib.dbag_attach_nccl(self._h, buf))
+
+    def round_phase(self, phase):
+        """External-transport round: phases 0, 1, 2 with exchange_copy between."""
+        rec = _capi.IterationRecord()
+        _check(self._lib.dbag_round_phase(self._h, phase, C.byref(rec) if phase == 2 else None))
+        return rec.as_dict() if phase == 2 else None
+
+    def exchange_copy(self, src, which):
+        _check(self._lib.dbag_exchange_copy(self._h, src._h, which))
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
@@ -392,6 +421,49 @@ class AdmmSolver:
 
     def reset_stats(self):
         _check(self._lib.dbag_reset_stats(self._h))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_capi.load().dbag_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def shard_plan(problem: Problem, rank: int, world: int) -> dict:
+    """Host-only shard plan (dbag_shard_plan_*): no GPU needed."""
+    lib = _capi.load()
+    pv = problem._view()
+    h = C.c_void_p()
+    info = _capi.ShardInfo()
+    _check(lib.dbag_shard_plan_create(C.byref(pv), rank, world, C.byref(h), C.byref(info)))
+    try:
+        d = info.as_dict()
+        out = {"info": d,
+               "cam_lo": np.zeros(world + 1, np.int32),
+               "local_obs": np.zeros(d["local_obs"], np.int64),
+               "local_points": np.zeros(d["local_points"], np.int32),
+               "bp_of_local": np.zeros(d["local_points"], np.int32),
+               "owner_of_local": np.zeros(d["local_points"], np.int8),
+               "gb_off": np.zeros(d["boundary_points"] + 1, np.int64),
+               "gmap": np.zeros(d["boundary_copies"], np.int64),
+               "send_obs_local": np.zeros(d["send_count"], np.int64)}
+        p = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+        _check(lib.dbag_shard_plan_arrays(
+            h, p(out["cam_lo"], C.c_int32), p(out["local_obs"], C.c_int64),
+            p(out["local_points"], C.c_int32), p(out["bp_of_local"], C.c_int32),
+            p(out["owner_of_local"], C.c_int8), p(out["gb_off"], C.c_int64),
+            p(out["gmap"], C.c_int64), p(out["send_obs_local"], C.c_int64)))
+    finally:
+        lib.dbag_shard_plan_destroy(h)
+    return out
+
+
+def partition_cameras(obs_per_camera, world):
+    c = np.ascontiguousarray(obs_per_camera, np.int64)
+    lo = np.zeros(world + 1, np.int32)
+    _check(_capi.load().dbag_partition_cameras(len(c), c.ctypes.data_as(_capi.I64P), world,
+                                               lo.ctypes.data_as(_capi.I32P)))
+    return lo
 
 
 def measure_fp64_peak(device=0):

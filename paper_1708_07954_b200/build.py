@@ -13,9 +13,17 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdbag.so")
 # (source, extra flags): the exact-numerics TU must not contract a*b+c into
 # FMA — it is a bit-for-bit twin of the oracle's arithmetic.
-SOURCES = [("dbag_capi.cu", []), ("dbag_exact.cu", ["-fmad=false"]), ("dbag_scenes.cpp", [])]
+NCCL_HOME = None
+for _p in sys.path + [os.path.join(sys.prefix, "lib", "python3.12", "site-packages")]:
+    _c = os.path.join(_p, "nvidia", "nccl")
+    if os.path.exists(os.path.join(_c, "include", "nccl.h")):
+        NCCL_HOME = _c
+        break
+NCCL_INC = ["-I", os.path.join(NCCL_HOME, "include")] if NCCL_HOME else []
+SOURCES = [("dbag_capi.cu", NCCL_INC), ("dbag_exact.cu", ["-fmad=false"]),
+           ("dbag_scenes.cpp", []), ("dbag_shard.cpp", [])]
 HEADERS = ["dbag_common.cuh", "dbag_local.cuh", "dbag_lbfgs.cuh", "dbag_consensus.cuh",
-           "dbag_index.cuh", "dbag_exact.h"]
+           "dbag_index.cuh", "dbag_exact.h", "dbag_shard.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -58,7 +66,11 @@ def build(force=False, verbose=False, extra=()):
         if verbose:
             sys.stderr.write(res.stderr)
         objs.append(obj)
-    cmd = [nvcc(), *ARCH, "-shared", *objs, "-o", LIB + ".tmp"]
+    if not NCCL_HOME:
+        raise RuntimeError("NCCL headers/library (nvidia/nccl in site-packages) not found")
+    ncclib = os.path.join(NCCL_HOME, "lib")
+    cmd = [nvcc(), *ARCH, "-shared", *objs, "-o", LIB + ".tmp", "-L", ncclib, "-l:libnccl.so.2",
+           "-Xlinker", "-rpath," + ncclib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

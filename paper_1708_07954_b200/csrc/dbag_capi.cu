@@ -15,6 +15,8 @@
 #include "dbag_common.cuh"
 #include "dbag_consensus.cuh"
 #include "dbag_exact.h"
+#include "dbag_shard.h"
+#include <nccl.h>
 #include "dbag_index.cuh"
 #include "dbag_local.cuh"
 #include "dbag_lbfgs.cuh"
@@ -102,6 +104,14 @@ struct dbag_solver {
   double* init_pose = nullptr;  // device [M][6], kept for dbag_reset
   double* init_pts = nullptr;   // device [N][3]
   dbag_round_stats stats{};
+  // totals (== local sizes on a single-GPU solver)
+  int64_t L_total = 0;
+  int32_t M_total = 0, N_total = 0;
+  // shard
+  int32_t world = 1, rank = 0, cam_begin = 0;
+  std::vector<int32_t> local_points;  // local -> global point id (sharded only)
+  ncclComm_t comm = nullptr;
+  bool sharded() const { return world > 1; }
 
   ~dbag_solver() {
     cudaSetDevice(device);
@@ -112,6 +122,7 @@ struct dbag_solver {
     for (auto& set : prof_ev)
       for (auto& e : set) cudaEventDestroy(e);
     if (h_rec) cudaFreeHost(h_rec);
+    if (comm) ncclCommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -173,22 +184,32 @@ struct dbag_solver {
 
   // One round: local -> camera consensus+dual -> point consensus+dual+metric
   // -> final reduction. Events bracket each kernel (ev[0]..ev[4]).
-  void enqueue_round(bool with_ref) {
-    cudaEvent_t* e = ev;
-    if (profiling) {
-      if (prof_used == prof_ev.size()) {
-        std::array<cudaEvent_t, 5> set{};
-        for (auto& x : set) CK(cudaEventCreate(&x));
-        prof_ev.push_back(set);
-      }
-      e = prof_ev[prof_used++].data();
-    }
+  void exchange(int which) {
+    if (!sharded()) return;
+    if (!comm) raise(DBAG_ERR_NCCL, "sharded solver without a transport: dbag_attach_nccl or phases");
+    ncclResult_t r;
+    if (which == 0)
+      r = ncclAllGather(S.send_buf, S.recv_buf, (size_t)S.max_send * 6, ncclDouble, comm, stream);
+    else
+      r = ncclAllGather(S.metric_part, S.metric_recv, kRecFields, ncclDouble, comm, stream);
+    if (r != ncclSuccess) raise(DBAG_ERR_NCCL, std::string("NCCL: ") + ncclGetErrorString(r));
+  }
+
+  // Phase 0: local solve, camera consensus+dual, pack boundary copies.
+  void phase0(cudaEvent_t* e) {
     reset_err();
     CK(cudaEventRecord(e[0], stream));
     launch_local(0, S.L);
     CK(cudaEventRecord(e[1], stream));
     launch_camera(kModeConsensus | kModeDual);
+    if (sharded() && S.send_count > 0) {
+      k_pack_send<<<grid_for(S.send_count, 256), 256, 0, stream>>>(S);
+      CK_LAUNCH();
+    }
     CK(cudaEventRecord(e[2], stream));
+  }
+  // Phase 1: point consensus+dual+metric, MSE, this rank's partial record.
+  void phase1(cudaEvent_t* e, bool with_ref) {
     launch_point(kModeConsensus | kModeDual, true);
     CK(cudaEventRecord(e[3], stream));
     if (with_ref) {
@@ -197,7 +218,35 @@ struct dbag_solver {
     }
     k_final<<<1, 1024, 0, stream>>>(S, n_pt_parts, with_ref ? n_mse_parts : 0);
     CK_LAUNCH();
+  }
+  // Phase 2: combine the ranks' partial records.
+  void phase2(cudaEvent_t* e) {
+    k_combine<<<1, 32, 0, stream>>>(S, sharded() ? S.metric_recv : S.metric_part, world, M_total,
+                                    N_total);
+    CK_LAUNCH();
     CK(cudaEventRecord(e[4], stream));
+  }
+
+  cudaEvent_t* round_events() {
+    if (!profiling) return ev;
+    if (prof_used == prof_ev.size()) {
+      std::array<cudaEvent_t, 5> set{};
+      for (auto& x : set) CK(cudaEventCreate(&x));
+      prof_ev.push_back(set);
+    }
+    return prof_ev[prof_used++].data();
+  }
+
+  // One round: local -> camera consensus+dual -> [boundary all-gather] ->
+  // point consensus+dual+metric -> partial record -> [all-gather] -> combine.
+  // Events bracket the kernels (e[0]..e[4]).
+  void enqueue_round(bool with_ref) {
+    cudaEvent_t* e = round_events();
+    phase0(e);
+    exchange(0);
+    phase1(e, with_ref);
+    exchange(1);
+    phase2(e);
     if (profiling)
       for (int k = 0; k < 5; ++k) CK(cudaEventRecord(ev[k], stream));
   }
@@ -244,7 +293,7 @@ struct dbag_solver {
     r.iter = iteration;
     r.sum_reproj_err = h_rec[kRecSumErr];
     r.mean_reproj_err = h_rec[kRecInfeasible] > 0.0 ? std::numeric_limits<double>::infinity()
-                                                    : h_rec[kRecSumErr] / (double)S.L;
+                                                    : h_rec[kRecSumErr] / (double)L_total;
     r.max_primal_x = h_rec[kRecMaxPx];
     r.max_primal_y = h_rec[kRecMaxPy];
     r.max_dual_x = h_rec[kRecMaxDx];
@@ -341,11 +390,9 @@ void dbag_options_default(dbag_options* o) {
   o->numerics = DBAG_NUMERICS_EXACT;
 }
 
-int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const dbag_options* opts,
-                dbag_solver** out) {
-  *out = nullptr;
-  auto* h = new dbag_solver();
-  const int rc = guarded([&] {
+static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_param_view* init,
+                        const dbag_options* opts) {
+  {
     const int M = P->num_cameras, N = P->num_points;
     const int64_t L = P->num_obs;
     if (M < 0 || N < 0 || L < 0) raise(DBAG_ERR_VALIDATION, "negative problem sizes");
@@ -437,6 +484,9 @@ int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const d
     S.err_block = dev_alloc<int64_t>(pool, 1);
     S.err_obs = dev_alloc<int64_t>(pool, 1);
     S.record = dev_alloc<double>(pool, kRecFields + 4);
+    S.metric_part = dev_alloc<double>(pool, kRecFields);
+    S.world = 1;
+    S.rank = 0;
     CK(cudaMemsetAsync(S.counters, 0, sizeof(unsigned long long) * 8 * kCounterStripes, st));
     CK(cudaMemsetAsync(S.cam_stats, 0, sizeof(double) * 2 * (size_t)M, st));
     const dbag_options& o = *opts;
@@ -568,6 +618,122 @@ int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const d
       raise(DBAG_ERR_VALIDATION, "block sizes must be >= 1");
     if (o.points_per_block != 1 || o.cameras_per_block != 1)
       raise(DBAG_ERR_UNSUPPORTED, "only (1,1) blocks are built on the device (SURVEY §8(f) row 1)");
+    h->L_total = L;
+    h->M_total = M;
+    h->N_total = N;
+  }
+}
+
+int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const dbag_options* opts,
+                dbag_solver** out) {
+  *out = nullptr;
+  auto* h = new dbag_solver();
+  const int rc = guarded([&] { create_impl(h, P, init, opts); });
+  if (rc != DBAG_OK) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return DBAG_OK;
+}
+
+int dbag_create_sharded(const dbag_problem_view* F, const dbag_param_view* init,
+                        const dbag_options* opts, int32_t rank, int32_t world,
+                        dbag_solver** out) {
+  *out = nullptr;
+  auto* h = new dbag_solver();
+  const int rc = guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world) raise(DBAG_ERR_VALIDATION, "bad rank/world");
+    if (init->num_cameras != F->num_cameras || init->num_points != F->num_points)
+      raise(DBAG_ERR_SIZE_MISMATCH, "init state sizes do not match the problem");
+    ShardPlan plan;
+    try {
+      plan = make_shard_plan(F->num_cameras, F->num_points, F->num_obs, F->obs_cam, F->obs_pt,
+                             rank, world);
+    } catch (const std::out_of_range& e) {
+      raise(DBAG_ERR_INDEX_OUT_OF_RANGE, e.what());
+    } catch (const std::exception& e) {
+      raise(DBAG_ERR_VALIDATION, e.what());
+    }
+    // the local sub-problem: this rank's cameras, their observations, the points they see
+    const int32_t lm = plan.cam_end - plan.cam_begin;
+    const int32_t ln = (int32_t)plan.local_points.size();
+    const int64_t ll = (int64_t)plan.local_obs.size();
+    std::vector<double> uv(2 * ll), pose(6 * (size_t)lm), f(lm), pts(3 * (size_t)ln),
+        ipose(6 * (size_t)lm), ipts(3 * (size_t)ln), if_(lm);
+    for (int64_t q = 0; q < ll; ++q) {
+      uv[2 * q] = F->obs_uv[2 * plan.local_obs[q]];
+      uv[2 * q + 1] = F->obs_uv[2 * plan.local_obs[q] + 1];
+    }
+    const double* init_f = init->cam_f ? init->cam_f : F->cam_f;
+    for (int32_t j = 0; j < lm; ++j) {
+      for (int k = 0; k < 6; ++k) {
+        pose[6 * j + k] = F->cam_pose[6 * (size_t)(plan.cam_begin + j) + k];
+        ipose[6 * j + k] = init->cam_pose[6 * (size_t)(plan.cam_begin + j) + k];
+      }
+      f[j] = F->cam_f[plan.cam_begin + j];
+      if_[j] = init_f[plan.cam_begin + j];
+    }
+    for (int32_t i = 0; i < ln; ++i)
+      for (int k = 0; k < 3; ++k) {
+        if (F->points) pts[3 * i + k] = F->points[3 * (size_t)plan.local_points[i] + k];
+        ipts[3 * i + k] = init->points[3 * (size_t)plan.local_points[i] + k];
+      }
+    dbag_problem_view lp{lm, ln, ll, plan.local_cam.data(), plan.local_pt.data(), uv.data(),
+                         pose.data(), f.data(), F->points ? pts.data() : nullptr};
+    dbag_param_view li{lm, ln, ipose.data(), if_.data(), ipts.data()};
+    create_impl(h, &lp, &li, opts);
+    h->L_total = F->num_obs;
+    h->M_total = F->num_cameras;
+    h->N_total = F->num_points;
+    h->comm_floats = plan.comm_floats;
+    h->world = world;
+    h->rank = rank;
+    h->cam_begin = plan.cam_begin;
+    h->local_points = plan.local_points;
+    DevState& S = h->S;
+    S.world = world;
+    S.rank = rank;
+    if (world > 1) {
+      auto& pool = h->pool;
+      cudaStream_t st = h->stream;
+      S.bp_of_local = dev_alloc<int32_t>(pool, ln);
+      S.owner_of_local = dev_alloc<int8_t>(pool, ln);
+      S.gb_off = dev_alloc<int64_t>(pool, plan.gb_off.size());
+      S.gmap = dev_alloc<int64_t>(pool, plan.gmap.size());
+      S.send_count = plan.send_count;
+      S.max_send = plan.max_send;
+      S.send_pos = dev_alloc<int32_t>(pool, plan.send_count);
+      S.send_buf = dev_alloc<double>(pool, 6 * (size_t)plan.max_send);
+      S.recv_buf = dev_alloc<double>(pool, 6 * (size_t)plan.max_send * world);
+      S.metric_recv = dev_alloc<double>(pool, (size_t)kRecFields * world);
+      CK(cudaMemsetAsync(S.send_buf, 0, sizeof(double) * 6 * plan.max_send, st));
+      CK(cudaMemcpyAsync(S.bp_of_local, plan.bp_of_local.data(), 4 * (size_t)ln,
+                         cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(S.owner_of_local, plan.owner_of_local.data(), (size_t)ln,
+                         cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(S.gb_off, plan.gb_off.data(), 8 * plan.gb_off.size(),
+                         cudaMemcpyHostToDevice, st));
+      if (!plan.gmap.empty())
+        CK(cudaMemcpyAsync(S.gmap, plan.gmap.data(), 8 * plan.gmap.size(), cudaMemcpyHostToDevice,
+                           st));
+      if (plan.send_count > 0) {
+        int64_t* d_so = nullptr;
+        int32_t* d_o2b = nullptr;
+        CK(cudaMalloc(&d_so, 8 * (size_t)plan.send_count));
+        CK(cudaMalloc(&d_o2b, 4 * (size_t)std::max<int64_t>(S.L, 1)));
+        CK(cudaMemcpyAsync(d_so, plan.send_obs_local.data(), 8 * (size_t)plan.send_count,
+                           cudaMemcpyHostToDevice, st));
+        k_send_pos<<<grid_for(S.L, 256), 256, 0, st>>>(S, d_so, d_o2b);
+        CK_LAUNCH();
+        k_send_pos2<<<grid_for(plan.send_count, 256), 256, 0, st>>>(S, d_so, d_o2b);
+        CK_LAUNCH();
+        CK(cudaStreamSynchronize(st));
+        cudaFree(d_so);
+        cudaFree(d_o2b);
+      }
+      CK(cudaStreamSynchronize(st));
+    }
   });
   if (rc != DBAG_OK) {
     delete h;
@@ -575,6 +741,66 @@ int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const d
   }
   *out = h;
   return DBAG_OK;
+}
+
+int dbag_nccl_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    ncclUniqueId u;
+    const ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) raise(DBAG_ERR_NCCL, std::string("NCCL: ") + ncclGetErrorString(r));
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+  });
+}
+
+int dbag_attach_nccl(dbag_solver* h, const uint8_t id[128]) {
+  return guarded([&] {
+    CK(cudaSetDevice(h->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    const ncclResult_t r = ncclCommInitRank(&h->comm, h->world, u, h->rank);
+    if (r != ncclSuccess) raise(DBAG_ERR_NCCL, std::string("NCCL: ") + ncclGetErrorString(r));
+  });
+}
+
+int dbag_round_phase(dbag_solver* h, int32_t phase, dbag_iteration_record* out) {
+  return guarded([&] {
+    CK(cudaSetDevice(h->device));
+    cudaEvent_t* e = h->ev;
+    if (phase == 0) {
+      h->phase0(e);
+    } else if (phase == 1) {
+      h->phase1(e, false);
+    } else if (phase == 2) {
+      if (!h->sharded()) {
+        // a single-GPU solver combines its own partial
+      }
+      h->phase2(e);
+      if (out) h->fill_record(out, false);
+      else ++h->iteration;
+    } else {
+      raise(DBAG_ERR_VALIDATION, "phase must be 0, 1 or 2");
+    }
+    h->sync();
+  });
+}
+
+int dbag_exchange_copy(dbag_solver* dst, dbag_solver* src, int32_t which) {
+  return guarded([&] {
+    if (dst->world != src->world || !dst->sharded())
+      raise(DBAG_ERR_VALIDATION, "exchange between solvers of different worlds");
+    CK(cudaSetDevice(dst->device));
+    if (which == 0) {
+      if (dst->S.max_send != src->S.max_send) raise(DBAG_ERR_VALIDATION, "plan mismatch");
+      const size_t n = (size_t)src->S.max_send * 6;
+      CK(cudaMemcpyAsync(dst->S.recv_buf + n * src->rank, src->S.send_buf, n * sizeof(double),
+                         cudaMemcpyDefault, dst->stream));
+    } else {
+      CK(cudaMemcpyAsync(dst->S.metric_recv + (size_t)kRecFields * src->rank, src->S.metric_part,
+                         kRecFields * sizeof(double), cudaMemcpyDefault, dst->stream));
+    }
+    dst->sync();
+  });
 }
 
 void dbag_destroy(dbag_solver* h) { delete h; }
@@ -678,14 +904,17 @@ int dbag_get_consensus(dbag_solver* h, double* cam_pose, double* cam_f, double* 
     CK(cudaMemcpyAsync(y.data(), S.ybar, sizeof(double) * y.size(), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(x.data(), S.xbar, sizeof(double4) * x.size(), cudaMemcpyDeviceToHost, h->stream));
     h->sync();
+    // a shard writes its own cameras/points at their global indices
     for (int j = 0; j < S.M; ++j) {
-      for (int k = 0; k < 6; ++k) cam_pose[6 * (size_t)j + k] = y[8 * (size_t)j + k];
-      if (cam_f) cam_f[j] = y[8 * (size_t)j + 6];
+      const size_t g = (size_t)(h->cam_begin + j);
+      for (int k = 0; k < 6; ++k) cam_pose[6 * g + k] = y[8 * (size_t)j + k];
+      if (cam_f) cam_f[g] = y[8 * (size_t)j + 6];
     }
     for (int i = 0; i < S.N; ++i) {
-      points[3 * (size_t)i] = x[i].x;
-      points[3 * (size_t)i + 1] = x[i].y;
-      points[3 * (size_t)i + 2] = x[i].z;
+      const size_t g = h->sharded() ? (size_t)h->local_points[i] : (size_t)i;
+      points[3 * g] = x[i].x;
+      points[3 * g + 1] = x[i].y;
+      points[3 * g + 2] = x[i].z;
     }
   });
 }
@@ -697,12 +926,15 @@ int dbag_set_consensus(dbag_solver* h, const double* cam_pose, const double* poi
     std::vector<double> y(8 * (size_t)S.M);
     std::vector<double4> x(S.N);
     for (int j = 0; j < S.M; ++j) {
-      for (int k = 0; k < 6; ++k) y[8 * (size_t)j + k] = cam_pose[6 * (size_t)j + k];
+      const size_t g = (size_t)(h->cam_begin + j);
+      for (int k = 0; k < 6; ++k) y[8 * (size_t)j + k] = cam_pose[6 * g + k];
       y[8 * (size_t)j + 6] = h->cam_f[j];
       y[8 * (size_t)j + 7] = 0.0;
     }
-    for (int i = 0; i < S.N; ++i)
-      x[i] = make_double4(points[3 * (size_t)i], points[3 * (size_t)i + 1], points[3 * (size_t)i + 2], 0.0);
+    for (int i = 0; i < S.N; ++i) {
+      const size_t g = h->sharded() ? (size_t)h->local_points[i] : (size_t)i;
+      x[i] = make_double4(points[3 * g], points[3 * g + 1], points[3 * g + 2], 0.0);
+    }
     CK(cudaMemcpyAsync(S.ybar, y.data(), sizeof(double) * y.size(), cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(S.xbar, x.data(), sizeof(double4) * x.size(), cudaMemcpyHostToDevice, h->stream));
     h->sync();
@@ -816,7 +1048,7 @@ int dbag_block_objective(dbag_solver* h, int64_t block, double* out) {
   });
 }
 
-int64_t dbag_ops_per_iteration(dbag_solver* h) { return 3 * h->S.L; }  // blocks + 2 copies each
+int64_t dbag_ops_per_iteration(dbag_solver* h) { return 3 * h->L_total; }  // blocks + 2 copies each
 int64_t dbag_comm_floats(dbag_solver* h) { return h->comm_floats; }
 
 int dbag_mean_reprojection_error(dbag_solver* h, double* out) {

@@ -54,6 +54,18 @@ struct DevState {
   int64_t* err_block;     // first block that raised (local_update_all)
   int64_t* err_obs;       // first infeasible observation (input order)
   double* record;         // DevRecord
+  double* metric_part;    // [kRecFields] this rank's partial record (raw sums)
+  // ---- multi-GPU shard (null/0 on a single-GPU solver) ----
+  int32_t world, rank;
+  int32_t* bp_of_local;   // [N] global boundary index of a local point, or -1
+  int8_t* owner_of_local; // [N] 1 if this rank counts the point in point-wise sums
+  int64_t* gb_off;        // [B+1] global boundary copy ranges (reference copy order)
+  int64_t* gmap;          // [G] recv slot of each global boundary copy
+  int32_t* send_pos;      // [send_count] point-major position of each send copy
+  int64_t send_count, max_send;
+  double* send_buf;       // [max_send][6] x(3) r(3)
+  double* recv_buf;       // [world * max_send][6]
+  double* metric_recv;    // [world][kRecFields]
 };
 
 constexpr int kCounterStripes = 64;

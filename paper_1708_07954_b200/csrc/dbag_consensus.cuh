@@ -109,18 +109,38 @@ __global__ void __launch_bounds__(kPtThreads) k_point(DevState S) {
     const int64_t beg = S.pt_off[i], end = S.pt_off[i + 1];
     double xb[3];
     if (MODE & kModeConsensus) {
-      // admm_solver.cpp:324-332: anchor = first copy, sequential accumulation
-      const PointRec& a = S.prec[beg];
-      const double anc[3] = {a.x0, a.x1, a.x2};
+      // admm_solver.cpp:324-332: anchor = first copy, sequential accumulation in
+      // copy order. A boundary point of a sharded solve reads all its copies
+      // (every rank's) from the all-gathered buffer, in the same global order.
       const double inv_rho = 1.0 / S.rho_x;
-      double acc[3] = {0.0, 0.0, 0.0};
-      for (int64_t p = beg; p < end; ++p) {
-        const PointRec& r = S.prec[p];
-        acc[0] += (r.x0 - anc[0]) + inv_rho * r.r0;
-        acc[1] += (r.x1 - anc[1]) + inv_rho * r.r1;
-        acc[2] += (r.x2 - anc[2]) + inv_rho * r.r2;
+      double anc[3], acc[3] = {0.0, 0.0, 0.0}, cnt;
+      const int bp = S.bp_of_local ? S.bp_of_local[i] : -1;
+      if (bp >= 0) {
+        const int64_t g0 = S.gb_off[bp], g1 = S.gb_off[bp + 1];
+        const double* a = S.recv_buf + 6 * S.gmap[g0];
+        anc[0] = a[0];
+        anc[1] = a[1];
+        anc[2] = a[2];
+        for (int64_t g = g0; g < g1; ++g) {
+          const double* c = S.recv_buf + 6 * S.gmap[g];
+          acc[0] += (c[0] - anc[0]) + inv_rho * c[3];
+          acc[1] += (c[1] - anc[1]) + inv_rho * c[4];
+          acc[2] += (c[2] - anc[2]) + inv_rho * c[5];
+        }
+        cnt = (double)(g1 - g0);
+      } else {
+        const PointRec& a = S.prec[beg];
+        anc[0] = a.x0;
+        anc[1] = a.x1;
+        anc[2] = a.x2;
+        for (int64_t p = beg; p < end; ++p) {
+          const PointRec& r = S.prec[p];
+          acc[0] += (r.x0 - anc[0]) + inv_rho * r.r0;
+          acc[1] += (r.x1 - anc[1]) + inv_rho * r.r1;
+          acc[2] += (r.x2 - anc[2]) + inv_rho * r.r2;
+        }
+        cnt = (double)(end - beg);
       }
-      const double cnt = (double)(end - beg);
       const double4 old = S.xbar[i];
 #pragma unroll
       for (int k = 0; k < 3; ++k) xb[k] = anc[k] + acc[k] / cnt;
@@ -193,6 +213,7 @@ __global__ void __launch_bounds__(256) k_mse(DevState S) {
     c += da * da + db * db + dg * dg + (t0 * t0 + t1 * t1 + t2 * t2);
   }
   for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < S.N; i += stride) {
+    if (S.owner_of_local && !S.owner_of_local[i]) continue;  // counted by its first copy's rank
     const double4 a = S.xbar[i];
     const double* b = S.ref_pts + 3 * i;
     const double d0 = a.x - b[0], d1 = a.y - b[1], d2 = a.z - b[2];
@@ -207,7 +228,7 @@ __global__ void __launch_bounds__(256) k_mse(DevState S) {
 }
 
 // Final reduction (one CTA, fixed order): K2 partials, K3 per-camera stats,
-// MSE partials -> DevRecord.
+// MSE partials -> this rank's partial record (raw sums) in S.metric_part.
 __global__ void __launch_bounds__(1024) k_final(DevState S, int n_pt_parts, int n_mse_parts) {
   __shared__ double smem[32 * 4];
   double s = 0.0, px = 0.0, dx = 0.0, inf = 0.0, py = 0.0, dy = 0.0, cm = 0.0, pm = 0.0;
@@ -234,15 +255,62 @@ __global__ void __launch_bounds__(1024) k_final(DevState S, int n_pt_parts, int 
   const double d = block_max<1024>(py, smem);
   const double e = block_max<1024>(dy, smem);
   if (threadIdx.x == 0) {
-    S.record[kRecSumErr] = sums[0];
-    S.record[kRecMaxPx] = a;
-    S.record[kRecMaxDx] = b;
-    S.record[kRecInfeasible] = c;
-    S.record[kRecMaxPy] = d;
-    S.record[kRecMaxDy] = e;
-    S.record[kRecCamMse] = S.M ? sums[1] / (6.0 * S.M) : 0.0;
-    S.record[kRecPtMse] = S.N ? sums[2] / (3.0 * S.N) : 0.0;
+    double* o = S.metric_part;
+    o[kRecSumErr] = sums[0];
+    o[kRecMaxPx] = a;
+    o[kRecMaxDx] = b;
+    o[kRecInfeasible] = c;
+    o[kRecMaxPy] = d;
+    o[kRecMaxDy] = e;
+    o[kRecCamMse] = sums[1];
+    o[kRecPtMse] = sums[2];
   }
+}
+
+// Combine the ranks' partial records (rank order) into the round's record.
+__global__ void k_combine(DevState S, const double* parts, int world, int32_t m_total,
+                          int32_t n_total) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double r[kRecFields];
+  for (int f = 0; f < kRecFields; ++f) r[f] = parts[f];
+  for (int w = 1; w < world; ++w) {
+    const double* p = parts + (int64_t)w * kRecFields;
+    r[kRecSumErr] += p[kRecSumErr];
+    r[kRecCamMse] += p[kRecCamMse];
+    r[kRecPtMse] += p[kRecPtMse];
+    r[kRecMaxPx] = fmax(r[kRecMaxPx], p[kRecMaxPx]);
+    r[kRecMaxPy] = fmax(r[kRecMaxPy], p[kRecMaxPy]);
+    r[kRecMaxDx] = fmax(r[kRecMaxDx], p[kRecMaxDx]);
+    r[kRecMaxDy] = fmax(r[kRecMaxDy], p[kRecMaxDy]);
+    r[kRecInfeasible] = fmax(r[kRecInfeasible], p[kRecInfeasible]);
+  }
+  r[kRecCamMse] = m_total ? r[kRecCamMse] / (6.0 * m_total) : 0.0;
+  r[kRecPtMse] = n_total ? r[kRecPtMse] / (3.0 * n_total) : 0.0;
+  for (int f = 0; f < kRecFields; ++f) S.record[f] = r[f];
+}
+
+// Pack this rank's boundary copies (x, r) for the all-gather.
+__global__ void k_pack_send(DevState S) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S.send_count) return;
+  const PointRec& r = S.prec[S.send_pos[s]];
+  double* o = S.send_buf + 6 * s;
+  o[0] = r.x0;
+  o[1] = r.x1;
+  o[2] = r.x2;
+  o[3] = r.r0;
+  o[4] = r.r1;
+  o[5] = r.r2;
+}
+
+// send slot -> point-major position (setup): obs2blk is the inverse of blk_obs.
+__global__ void k_send_pos(DevState S, const int64_t* send_obs_local, int32_t* obs2blk) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < S.L) obs2blk[S.blk_obs[b]] = (int32_t)b;
+}
+__global__ void k_send_pos2(DevState S, const int64_t* send_obs_local, const int32_t* obs2blk) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < S.send_count) S.send_pos[s] = S.blk_pos[obs2blk[send_obs_local[s]]];
 }
 
 // ---- queries ---------------------------------------------------------------
