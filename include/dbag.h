@@ -26,6 +26,7 @@
 #ifndef DBAG_H_
 #define DBAG_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -46,7 +47,8 @@ typedef enum {
   DBAG_ERR_INDEX_OUT_OF_RANGE = 7, /* IndexOutOfRange                    */
   DBAG_ERR_DUPLICATE_OBSERVATION = 8, /* DuplicateObservation            */
   DBAG_ERR_UNSUPPORTED = 9,     /* valid for the reference, not built here */
-  DBAG_ERR_GENERIC = 10         /* Error (e.g. "local block N: ...")     */
+  DBAG_ERR_GENERIC = 10,        /* Error (e.g. "local block N: ...")     */
+  DBAG_ERR_PARSE = 11           /* ParseError (a ValidationError) with line */
 } dbag_status;
 
 typedef enum { DBAG_LOSS_SQUARED_L2 = 0, DBAG_LOSS_HUBER = 1 } dbag_loss; /* losses.hpp:13-29 */
@@ -250,6 +252,24 @@ int dbag_attach_nccl(dbag_solver* h, const uint8_t id[128]);
  *   phase 2: combine -> *out (only for phase 2; may be NULL otherwise). */
 int dbag_round_phase(dbag_solver* h, int32_t phase, dbag_iteration_record* out);
 int dbag_exchange_copy(dbag_solver* dst, dbag_solver* src, int32_t which);
+
+/* ---- problem files and metrics CSV (bal_io.hpp:21-31, metrics_csv.hpp:11-19)
+ * Host-only. parse: the reference's text format (optional `rotation euler|
+ * angle-axis` header; m n l; l observation lines; 9 values per camera with zero
+ * distortion; 3 per point) followed by Problem::create validation. serialize:
+ * 17 significant digits (bit-exact round trip), observations from `problem`,
+ * cameras/points from `state`. Two-phase outputs: buf NULL -> *len only. */
+typedef struct dbag_bal dbag_bal;
+int dbag_parse_problem_text(const char* text, size_t len, dbag_bal** out, int32_t* m,
+                            int32_t* n, int64_t* l);
+int dbag_bal_fetch(const dbag_bal* b, int32_t* obs_cam, int32_t* obs_pt, double* obs_uv,
+                   double* cam_pose, double* cam_f, double* points);
+void dbag_bal_destroy(dbag_bal* b);
+int dbag_serialize_problem_text(const dbag_problem_view* problem, const dbag_param_view* state,
+                                char* buf, size_t cap, size_t* len);
+int dbag_metrics_csv(const dbag_iteration_record* trace, int64_t n, char* buf, size_t cap,
+                     size_t* len);
+const char* dbag_io_last_error(int32_t* line); /* message and ParseError line (-1: none) */
 
 /* Synthetic scenes of BASELINE.json configs 1-5 (host C++, deterministic in
  * seed). Two-phase: size query, then fill. scale in (0,1]

@@ -4,7 +4,8 @@ host mirror of the reference AdmmSolver API (admm.py)."""
 from .admm import (AdmmOptions, AdmmSolver, AdmmState, DepthBelowGuard, DeviceError,  # noqa
                    DuplicateObservation, Error, IndexOutOfRange, InnerOptions, LossKind,
                    ParamState, Problem, Scene, SingularSystem, SizeMismatch, Unsupported,
-                   ValidationError, generate_config_scene, run_admm)
+                   ValidationError, generate_config_scene, run_admm, ParseError,
+                   parse_problem_text, serialize_problem_text, metrics_csv)
 from ._capi import load as load_library  # noqa: F401
 
 __all__ = ["AdmmOptions", "AdmmSolver", "AdmmState", "ParamState", "Problem", "LossKind",

@@ -130,6 +130,14 @@ SIGNATURES = {
     "dbag_attach_nccl": (C.c_int, [H, U8P]),
     "dbag_round_phase": (C.c_int, [H, C.c_int32, C.POINTER(IterationRecord)]),
     "dbag_exchange_copy": (C.c_int, [H, H, C.c_int32]),
+    "dbag_parse_problem_text": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(H), I32P, I32P, I64P]),
+    "dbag_bal_fetch": (C.c_int, [H, I32P, I32P, DPTR, DPTR, DPTR, DPTR]),
+    "dbag_bal_destroy": (None, [H]),
+    "dbag_serialize_problem_text": (C.c_int, [C.POINTER(ProblemView), C.POINTER(ParamView),
+                                              C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "dbag_metrics_csv": (C.c_int, [C.POINTER(IterationRecord), C.c_int64, C.c_char_p, C.c_size_t,
+                                   C.POINTER(C.c_size_t)]),
+    "dbag_io_last_error": (C.c_char_p, [I32P]),
     "dbag_scene_generate": (C.c_int, [C.c_int32, C.c_uint64, C.c_double, C.POINTER(H),
                                       C.POINTER(SceneInfo)]),
     "dbag_scene_fetch": (C.c_int, [H, I32P, I32P, DPTR, DPTR, DPTR, DPTR, DPTR, DPTR]),

@@ -47,6 +47,14 @@ class SingularSystem(Error):
     pass
 
 
+class ParseError(ValidationError):
+    """dba::ParseError (errors.hpp:16-22): carries the 1-based line."""
+
+    def __init__(self, msg, line=-1):
+        super().__init__(msg)
+        self.line = line
+
+
 class DeviceError(Error):
     """CUDA / NCCL failure (no reference analogue)."""
 
@@ -421,6 +429,65 @@ class AdmmSolver:
 
     def reset_stats(self):
         _check(self._lib.dbag_reset_stats(self._h))
+
+
+# ---- problem files and metrics CSV (bal_io.hpp:21-31, metrics_csv.hpp:11-19) -----
+
+
+def _io_check(rc):
+    if rc == 0:
+        return
+    line = C.c_int32()
+    msg = _capi.load().dbag_io_last_error(C.byref(line)).decode()
+    if rc == 11:
+        raise ParseError(msg, line.value)
+    raise _STATUS.get(rc, Error)(msg)
+
+
+def parse_problem_text(text: str):
+    """bal_io.cpp:100-185 -> (Problem, init ParamState)."""
+    lib = _capi.load()
+    raw = text.encode()
+    h = C.c_void_p()
+    m, n, l = C.c_int32(), C.c_int32(), C.c_int64()
+    _io_check(lib.dbag_parse_problem_text(raw, len(raw), C.byref(h), C.byref(m), C.byref(n),
+                                          C.byref(l)))
+    try:
+        cam, pt = np.zeros(l.value, np.int32), np.zeros(l.value, np.int32)
+        uv, pose = np.zeros((l.value, 2)), np.zeros((m.value, 6))
+        f, pts = np.zeros(m.value), np.zeros((n.value, 3))
+        lib.dbag_bal_fetch(h, _ip(cam), _ip(pt), _dp(uv), _dp(pose), _dp(f), _dp(pts))
+    finally:
+        lib.dbag_bal_destroy(h)
+    return Problem(cam, pt, uv, pose, f, pts), ParamState(pose.copy(), f.copy(), pts.copy())
+
+
+def serialize_problem_text(problem: Problem, state: ParamState) -> str:
+    """bal_io.cpp:197-231 (17 significant digits: bit-exact round trip)."""
+    lib = _capi.load()
+    st = state.copy()
+    pv, sv = problem._view(), st._view()
+    n = C.c_size_t()
+    _io_check(lib.dbag_serialize_problem_text(C.byref(pv), C.byref(sv), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _io_check(lib.dbag_serialize_problem_text(C.byref(pv), C.byref(sv), buf, n.value + 1,
+                                              C.byref(n)))
+    return buf.value.decode()
+
+
+def metrics_csv(trace) -> str:
+    """metrics_csv.cpp:16-38 for a list of iterate()/run() records."""
+    recs = (_capi.IterationRecord * max(1, len(trace)))()
+    for k, r in enumerate(trace):
+        for name, _ in _capi.IterationRecord._fields_:
+            if name in r:
+                setattr(recs[k], name, r[name])
+    n = C.c_size_t()
+    lib = _capi.load()
+    _io_check(lib.dbag_metrics_csv(recs, len(trace), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _io_check(lib.dbag_metrics_csv(recs, len(trace), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
 
 
 def nccl_unique_id() -> bytes:

@@ -472,3 +472,24 @@ def test_cpp_dropin_driver_matches_oracle(O, P):
         assert float(f[2]) == o["max_primal_x"] and float(f[3]) == o["max_primal_y"]
         assert rel_close(float(f[1]), o["mean_reproj_err"], 1e-12)
         assert int(f[7]) == o["comm_floats"]
+
+
+def test_cpp_driver_file_mode_round_trip(O, P, tmp_path):
+    """`dbag_solve file`: parse a reference problem file, solve on the device,
+    write the solved file + metrics CSV; the solved state equals the oracle's."""
+    import subprocess
+    from paper_1708_07954_b200 import build as b
+    arrays, init = orbit_arrays(O, 93, 0.01, 0.01)
+    prob = P.Problem.create(*arrays)
+    src = tmp_path / "p.txt"
+    src.write_text(P.serialize_problem_text(prob, P.ParamState(init[0], arrays[1], init[1])))
+    out, csv = tmp_path / "s.txt", tmp_path / "m.csv"
+    r = subprocess.run([b.TOOL_BIN, "file", str(src), "15", "l2", "exact", str(out), str(csv)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    _, solved = P.parse_problem_text(out.read_text())
+    _, osol, _ = pair(O, P, arrays, init, max_iters=15)
+    osol.run()
+    opose, _, opts = osol.consensus()
+    assert np.array_equal(solved.cam_pose, opose) and np.array_equal(solved.points, opts)
+    assert csv.read_text().count("\n") == 16

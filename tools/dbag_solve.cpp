@@ -1,16 +1,91 @@
 // dbag_solve — C++ host driver over the drop-in header (include/dbag.hpp):
 // what `dba solve --solver admm` (tools/dba_main.cpp:231-259) does, on the B200.
-// Generates a BASELINE config scene, runs run_admm, prints the trace in the
-// reference's metrics CSV schema (metrics_csv.hpp:11-12).
 //   dbag_solve <config 1..5> <rounds> [l2|huber] [exact|fast] [scale]
+//       generate a BASELINE config scene, solve, print the metrics CSV
+//   dbag_solve file <problem.txt> <rounds> [l2|huber] [exact|fast] [solved.txt] [metrics.csv]
+//       parse a reference problem file (bal_io.hpp format), solve from its
+//       record, write the solved problem and the metrics CSV (metrics_csv.hpp)
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
 #include <vector>
 
 #include "dbag.hpp"
 
+static int solve_file(int argc, char** argv) {
+  if (argc < 4) return 2;
+  std::ifstream in(argv[2], std::ios::binary);
+  if (!in) {
+    std::fprintf(stderr, "cannot open '%s'\n", argv[2]);
+    return 3;
+  }
+  std::ostringstream ss;
+  ss << in.rdbuf();
+  const std::string text = ss.str();
+  dbag_bal* b = nullptr;
+  int32_t m = 0, n = 0;
+  int64_t l = 0;
+  if (dbag_parse_problem_text(text.data(), text.size(), &b, &m, &n, &l) != DBAG_OK) {
+    int32_t line = -1;
+    std::fprintf(stderr, "data error: %s\n", dbag_io_last_error(&line));
+    return 3;
+  }
+  dba::gpu::Problem problem;
+  problem.obs_cam.resize(l);
+  problem.obs_pt.resize(l);
+  problem.obs_uv.resize(2 * l);
+  problem.nominal.cam_pose.resize(6 * m);
+  problem.nominal.cam_f.resize(m);
+  problem.nominal.points.resize(3 * n);
+  dbag_bal_fetch(b, problem.obs_cam.data(), problem.obs_pt.data(), problem.obs_uv.data(),
+                 problem.nominal.cam_pose.data(), problem.nominal.cam_f.data(),
+                 problem.nominal.points.data());
+  dbag_bal_destroy(b);
+  dba::gpu::AdmmOptions opts;
+  opts.max_iters = std::atoi(argv[3]);
+  opts.misfit_loss = argc > 4 && std::strcmp(argv[4], "huber") == 0
+                         ? dba::gpu::LossKind::huber(1.0)
+                         : dba::gpu::LossKind::squared_l2();
+  opts.numerics = argc > 5 && std::strcmp(argv[5], "fast") == 0 ? DBAG_NUMERICS_FAST
+                                                                 : DBAG_NUMERICS_EXACT;
+  try {
+    const dba::gpu::AdmmResult res = dba::gpu::run_admm(problem, problem.nominal_state(), opts);
+    auto write = [](const char* path, auto fill) {
+      size_t len = 0;
+      fill(nullptr, 0, &len);
+      std::string buf(len + 1, '\0');
+      fill(buf.data(), buf.size(), &len);
+      std::ofstream out(path, std::ios::binary | std::ios::trunc);
+      out.write(buf.data(), (std::streamsize)len);
+    };
+    if (argc > 6) {
+      const dbag_problem_view pv = problem.view();
+      const dbag_param_view sv = res.state.view();
+      write(argv[6], [&](char* o, size_t c, size_t* len) {
+        dbag_serialize_problem_text(&pv, &sv, o, c, len);
+      });
+    }
+    if (argc > 7)
+      write(argv[7], [&](char* o, size_t c, size_t* len) {
+        dbag_metrics_csv(res.trace.data(), (int64_t)res.trace.size(), o, c, len);
+      });
+    std::printf("rounds=%zu final_mean_reproj_err=%.17g\n", res.trace.size(),
+                res.trace.empty() ? 0.0 : res.trace.back().mean_reproj_err);
+  } catch (const dba::gpu::ValidationError& e) {
+    std::fprintf(stderr, "data error: %s\n", e.what());
+    return 3;
+  } catch (const dba::gpu::Error& e) {
+    std::fprintf(stderr, "solver error: %s\n", e.what());
+    return 4;
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::strcmp(argv[1], "file") == 0) return solve_file(argc, argv);
   const int config = argc > 1 ? std::atoi(argv[1]) : 1;
   const int rounds = argc > 2 ? std::atoi(argv[2]) : 50;
   const bool huber = argc > 3 && std::strcmp(argv[3], "huber") == 0;
