@@ -91,6 +91,59 @@ __device__ __forceinline__ void trig_of(double a, double b, double g, Trig& t) {
   sincos(g, &t.sg, &t.cg);
 }
 
+// FAST numerics helpers (never used by the EXACT kernels) ---------------------
+// 1/x to ~1 ulp: MUFU.RCP64H seed + two Newton steps, branch-free.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// sin and cos of |x| <= 1e5 (the Euler angles): Cody-Waite reduction by pi/2
+// with FMA, Taylor polynomials to x^17 / x^18 on [-pi/4, pi/4], branch-free
+// quadrant select; ~1 ulp. Straight-line code, so three calls interleave.
+__device__ __forceinline__ void fast_sincos(double x, double* sn, double* cs) {
+  const double k = rint(x * 0.6366197723675814);
+  double r = fma(-k, 1.5707963267948966, x);
+  r = fma(-k, 6.123233995736766e-17, r);
+  const double z = r * r;
+  double p = 2.8114572543455206e-15;
+  p = fma(p, z, -7.647163731819816e-13);
+  p = fma(p, z, 1.6059043836821613e-10);
+  p = fma(p, z, -2.505210838544172e-08);
+  p = fma(p, z, 2.7557319223985893e-06);
+  p = fma(p, z, -0.0001984126984126984);
+  p = fma(p, z, 0.008333333333333333);
+  p = fma(p, z, -0.16666666666666666);
+  const double s = fma(r * z, p, r);
+  double q = -1.5619206968586225e-16;
+  q = fma(q, z, 4.779477332387385e-14);
+  q = fma(q, z, -1.1470745597729725e-11);
+  q = fma(q, z, 2.08767569878681e-09);
+  q = fma(q, z, -2.755731922398589e-07);
+  q = fma(q, z, 2.48015873015873e-05);
+  q = fma(q, z, -0.001388888888888889);
+  q = fma(q, z, 0.041666666666666664);
+  const double c = fma(z * z, q, fma(-0.5, z, 1.0));
+  const int n = static_cast<int>(static_cast<long long>(k) & 3);
+  const double s1 = (n & 1) ? c : s, c1 = (n & 1) ? s : c;
+  *sn = (n & 2) ? -s1 : s1;
+  *cs = ((n + 1) & 2) ? -c1 : c1;
+}
+
+__device__ __forceinline__ void fast_trig_of(double a, double b, double g, Trig& t) {
+  if (fabs(a) < 1e5 && fabs(b) < 1e5 && fabs(g) < 1e5) {
+    fast_sincos(a, &t.sa, &t.ca);
+    fast_sincos(b, &t.sb, &t.cb);
+    fast_sincos(g, &t.sg, &t.cg);
+  } else {
+    trig_of(a, b, g, t);
+  }
+}
+
 __device__ __forceinline__ void rot_of(const Trig& t, double R[9]) {
   const double m01 = -t.sg, m02 = t.cg * t.sb;
   const double m11 = t.cg, m12 = t.sg * t.sb;

@@ -43,24 +43,27 @@ __device__ __forceinline__ void flush_counters(const DevState& S, const LocalCou
 // r = [z - pi(v) ; wx (v_x - tx) ; wy (v_y - ty)], objective ||r||^2 summed in
 // row order. Returns false when the projection is infeasible.
 struct GnProblem {
-  double tgt[9];   // x~ (3) and y~ (6): completed-square targets (:152-164)
+  double* tgt;     // x~ (3) and y~ (6), completed-square targets (:152-164), in
+                   // shared memory with stride blockDim (keeps them out of spills)
   double z0, z1, f, wx, wy, eps;
+  __device__ __forceinline__ double T(int k) const { return tgt[k * 128]; }
 };
 
 __device__ __forceinline__ bool gn_residual(const GnProblem& P, const double v[9], Trig& tr,
                                             double R[9], double w[3], double& e0, double& e1,
                                             double& obj) {
-  trig_of(v[3], v[4], v[5], tr);
+  fast_trig_of(v[3], v[4], v[5], tr);
   rot_of(tr, R);
   cam_point(R, v, v + 6, w);
   if (!feasible(w[2], P.eps)) return false;
-  e0 = P.z0 - P.f * w[0] / w[2];
-  e1 = P.z1 - P.f * w[1] / w[2];
+  const double iw = fast_rcp(w[2]);
+  e0 = P.z0 - P.f * w[0] * iw;
+  e1 = P.z1 - P.f * w[1] * iw;
   double s = e0 * e0 + e1 * e1;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     const double wk = k < 3 ? P.wx : P.wy;
-    const double rk = wk * (v[k] - P.tgt[k]);
+    const double rk = wk * (v[k] - P.T(k));
     s += rk * rk;
   }
   obj = s;
@@ -73,7 +76,7 @@ __device__ __forceinline__ bool gn_residual(const GnProblem& P, const double v[9
 __device__ __forceinline__ void proj_jacobian(const double v[9], const Trig& t, const double R[9],
                                               const double w[3], double f, double A0[9],
                                               double A1[9]) {
-  const double inv_z = 1.0 / w[2];
+  const double inv_z = fast_rcp(w[2]);
   const double a = f * inv_z;
   const double b0 = -f * w[0] * inv_z * inv_z;
   const double b1 = -f * w[1] * inv_z * inv_z;
@@ -122,6 +125,7 @@ __device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, 
       !isfinite(obj))
     return false;
   const double wx2 = P.wx * P.wx, wy2 = P.wy * P.wy;
+  const double iwx2 = 1.0 / wx2, iwy2 = 1.0 / wy2;  // D^-1 of the undamped first trial
   for (int it = 0; it < S.inner_max_iters; ++it) {
     // J = [-A ; diag(w)] at v
     double A0[9], A1[9];
@@ -131,7 +135,7 @@ __device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, 
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
       const double wk = k < 3 ? P.wx : P.wy;
-      const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.tgt[k]));
+      const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.T(k)));
       rhs[k] = -jtr;                 // -0.5 g
       const double gk = 2.0 * jtr;   // g = 2 J^T r
       g2 += gk * gk;
@@ -145,12 +149,12 @@ __device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, 
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
         const double wk2 = k < 3 ? wx2 : wy2;
-        double Dk = wk2;
         if (lambda > 0.0) {
           const double hkk = (A0[k] * A0[k] + A1[k] * A1[k]) + wk2;
-          Dk = wk2 + lambda * fmax(hkk, 1e-12);
+          iD[k] = fast_rcp(wk2 + lambda * fmax(hkk, 1e-12));
+        } else {
+          iD[k] = k < 3 ? iwx2 : iwy2;
         }
-        iD[k] = __drcp_rn(Dk);
         u[k] = rhs[k] * iD[k];
         c00 += A0[k] * A0[k] * iD[k];
         c01 += A0[k] * A1[k] * iD[k];
@@ -158,9 +162,9 @@ __device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, 
         a0 += A0[k] * u[k];
         a1 += A1[k] * u[k];
       }
-      const double det = c00 * c11 - c01 * c01;
-      const double y0 = (c11 * a0 - c01 * a1) / det;
-      const double y1 = (c00 * a1 - c01 * a0) / det;
+      const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
+      const double y0 = (c11 * a0 - c01 * a1) * idet;
+      const double y1 = (c00 * a1 - c01 * a0) * idet;
       double vt[9], d2 = 0.0;
       bool fin = true;
 #pragma unroll
@@ -209,6 +213,7 @@ __device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, 
 // K1 entry: blocks [begin, begin+count) in block order.
 template <int kLoss>
 __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local(DevState S, int64_t begin, int64_t count) {
+  __shared__ double tgt_s[9 * 128];
   const int64_t b = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   LocalCounters cnt;
   if (b < begin + count) {
@@ -230,12 +235,13 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local(DevState S, int64_t
     bool ok;
     if (kLoss == 0) {
       GnProblem P;
+      P.tgt = tgt_s + threadIdx.x;
       // completed-square targets x~ = xbar - r/rho, y~ = ybar - s/rho (:152-164)
       P.tgt[0] = xb.x - rec.r0 / S.rho_x;
-      P.tgt[1] = xb.y - rec.r1 / S.rho_x;
-      P.tgt[2] = xb.z - rec.r2 / S.rho_x;
+      P.tgt[128] = xb.y - rec.r1 / S.rho_x;
+      P.tgt[256] = xb.z - rec.r2 / S.rho_x;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) P.tgt[3 + k] = yb[k] - sd[k] / S.rho_y;
+      for (int k = 0; k < 6; ++k) P.tgt[(3 + k) * 128] = yb[k] - sd[k] / S.rho_y;
       P.z0 = rec.u;
       P.z1 = rec.v;
       P.f = yb[6];

@@ -12,7 +12,9 @@ VARIANTS = {
     "base": [],
     "fast_minb3": ["-DDBAG_K1_MINB=3"],
     "fast_minb4": ["-DDBAG_K1_MINB=4"],
+    "exact_minb2": ["-DDBAG_K1E_MINB=2"],
     "exact_minb3": ["-DDBAG_K1E_MINB=3"],
+    "exact_minb4": ["-DDBAG_K1E_MINB=4"],
 }
 
 
