@@ -172,11 +172,12 @@ struct dbag_solver {
       CK(exact::launch_local(S, begin, count, stream));
       return;
     }
-    const unsigned g = grid_for(count, 128);
-    if (opts.loss == DBAG_LOSS_SQUARED_L2)
-      k_local<0><<<g, 128, 0, stream>>>(S, begin, count);
-    else
-      k_local_huber<<<g, kHuberThreads, 0, stream>>>(S, begin, count);
+    if (opts.loss == DBAG_LOSS_SQUARED_L2) {
+      k_local<0><<<grid_for(count, 128), 128, 0, stream>>>(S, begin, count);
+      CK_LAUNCH();
+      return;
+    }
+    k_local_huber<<<grid_for(count, kHuberThreads), kHuberThreads, 0, stream>>>(S, begin, count);
     CK_LAUNCH();
   }
 
@@ -485,6 +486,8 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     S.err_obs = dev_alloc<int64_t>(pool, 1);
     S.record = dev_alloc<double>(pool, kRecFields + 4);
     S.metric_part = dev_alloc<double>(pool, kRecFields);
+    S.work = dev_alloc<unsigned long long>(pool, 1);
+
     S.world = 1;
     S.rank = 0;
     CK(cudaMemsetAsync(S.counters, 0, sizeof(unsigned long long) * 8 * kCounterStripes, st));

@@ -55,6 +55,7 @@ struct DevState {
   int64_t* err_obs;       // first infeasible observation (input order)
   double* record;         // DevRecord
   double* metric_part;    // [kRecFields] this rank's partial record (raw sums)
+  unsigned long long* work;  // K1 work counter (zeroed before each launch)
   // ---- multi-GPU shard (null/0 on a single-GPU solver) ----
   int32_t world, rank;
   int32_t* bp_of_local;   // [N] global boundary index of a local point, or -1
@@ -69,6 +70,25 @@ struct DevState {
 };
 
 constexpr int kCounterStripes = 64;
+
+// Lane-level work refill for persistent K1 kernels: every idle lane of the
+// warp takes the next observation index (one atomic per warp). Returns the
+// lane's new index or -1 when the work is exhausted.
+__device__ __forceinline__ int64_t refill(const DevState& S, bool idle, int64_t count,
+                                          bool& exhausted) {
+  const unsigned full = 0xffffffffu;
+  const unsigned m = __ballot_sync(full, idle && !exhausted);
+  if (m == 0) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(S.work, (unsigned long long)__popc(m));
+  base = __shfl_sync(full, base, leader);
+  if (base + __popc(m) >= (unsigned long long)count) exhausted = true;
+  if (!(m & (1u << lane))) return -1;
+  const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
+  return idx < (unsigned long long)count ? (int64_t)idx : -1;
+}
 
 // DevRecord layout (doubles)
 enum RecField {
