@@ -298,6 +298,37 @@ def our_arm(args, rank, world, local_rank):
         ms_total = float(t.item())
     stats = solver.round_stats()
     last = solver.iterate()  # one more round with the metrics read back (untimed)
+
+    # the other numerics mode, same rounds 1..K from the same init (reported
+    # beside the headline; DESIGN.md §5 explains the two modes)
+    other = "fast" if args.numerics == "exact" else "exact"
+    o_opts = P.AdmmOptions(misfit_loss=loss, max_iters=10 ** 9, device=dev,
+                           numerics=P.admm.FAST if other == "fast" else P.admm.EXACT)
+    solver2 = make(p, scene.init, o_opts)
+    solver2.enqueue_round()
+    solver2.synchronize()
+    solver2.reset()
+    stream2 = torch.cuda.ExternalStream(solver2.stream_handle(), device=dev)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    f0.record(stream2)
+    for _ in range(args.steps):
+        solver2.enqueue_round()
+    f1.record(stream2)
+    solver2.synchronize()
+    ms2 = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([ms2], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms2 = float(t.item())
+    solver2.close()
+    other_line = {"numerics": other, "value": L * args.steps / (ms2 / 1e3),
+                  "ms_per_step": ms2 / args.steps,
+                  "note": ("FMA, Woodbury 2x2 solve, hardware-style sin/cos: same algorithm and "
+                           "control flow, last-ulp rounding differs (trajectory not bit-identical)"
+                           if other == "fast" else
+                           "bit-identical to the restated reference (oracle/)")}
     value = L * args.steps / (ms_total / 1e3)  # whole job: every rank's share of one scene
 
     # ---------------- roofline
@@ -360,6 +391,7 @@ def our_arm(args, rank, world, local_rank):
                     "scope": f"dbag_create (H2D + device index build) + {args.steps} rounds "
                              f"(record D2H each) + consensus D2H, wall clock"},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu,
+            "other_numerics": other_line,
             "clocks": clocks.summary(),
             "gpu_launches": (6 if world > 1 else 4) * args.steps,
             "counters": {k: stats[k] for k in ("n_jacobian", "n_trial", "n_accept",
