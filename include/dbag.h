@@ -93,7 +93,8 @@ typedef struct {
   int32_t max_line_search;
   double eps_depth;
   int32_t workers;         /* validated >= 1 (reference semantics); unused on GPU */
-  int32_t points_per_block, cameras_per_block; /* only (1,1) is built */
+  int32_t points_per_block, cameras_per_block; /* BlockConfig (admm_solver.hpp:29-32);
+                                                 * != (1,1): generalized blocks, EXACT numerics */
   int32_t device;          /* CUDA device ordinal */
   int32_t numerics;        /* dbag_numerics */
 } dbag_options;
@@ -175,7 +176,19 @@ int dbag_set_copies(dbag_solver* h, const double* local_points, const double* lo
                     const double* dual_r, const double* dual_s);
 int32_t dbag_iteration(dbag_solver* h);
 int64_t dbag_num_blocks(dbag_solver* h);
-int dbag_get_block_order(dbag_solver* h, int32_t* obs_ids /*[l]*/); /* blocks()[b].obs_ids[0] */
+/* observation ids of all blocks, concatenated in block order (== sorted by
+ * (cam_id, point_id), admm_solver.cpp:19-27) */
+int dbag_get_block_order(dbag_solver* h, int32_t* obs_ids /*[l]*/);
+/* copy counts: sum of |point_ids| / |cam_ids| over blocks (== l for (1,1)).
+ * dbag_get_copies / dbag_set_copies take [point_copies][3], [cam_copies][6],
+ * [point_copies][3], [cam_copies][6], block by block in id order. */
+int dbag_num_copies(dbag_solver* h, int64_t* point_copies, int64_t* cam_copies);
+/* blocks() (admm_solver.hpp:102-108, LocalBlock admm_solver.hpp:35-45): CSR over
+ * blocks; every pointer nullable. obs_off/pt_off/cam_off [B+1], pt_ids [PC],
+ * cam_ids [CC], obs_*_local [l] (in block order). */
+int dbag_get_blocks(dbag_solver* h, int64_t* obs_off, int64_t* pt_off, int32_t* pt_ids,
+                    int64_t* cam_off, int32_t* cam_ids, int32_t* obs_pt_local,
+                    int32_t* obs_cam_local);
 
 /* Result/objective queries (admm_solver.hpp:110-127). */
 int dbag_max_primal(dbag_solver* h, double* max_x, double* max_y);
@@ -259,6 +272,19 @@ int dbag_exchange_copy(dbag_solver* dst, dbag_solver* src, int32_t which);
  * distortion; 3 per point) followed by Problem::create validation. serialize:
  * 17 significant digits (bit-exact round trip), observations from `problem`,
  * cameras/points from `state`. Two-phase outputs: buf NULL -> *len only. */
+/* ---- host-only: partition() and communication_cost() (admm_solver.hpp:47-54,
+ * admm_solver.cpp:14-101) for any BlockConfig. No GPU needed. */
+typedef struct dbag_partition_result dbag_partition_result;
+int dbag_partition(const dbag_problem_view* problem, int32_t points_per_block,
+                   int32_t cameras_per_block, dbag_partition_result** out, int64_t* n_blocks,
+                   int64_t* n_point_copies, int64_t* n_cam_copies, int64_t* comm_floats);
+int dbag_partition_fetch(const dbag_partition_result* r, int64_t* obs_off /*[B+1]*/,
+                         int32_t* obs_ids /*[l]*/, int64_t* pt_off /*[B+1]*/,
+                         int32_t* pt_ids /*[PC]*/, int64_t* cam_off /*[B+1]*/,
+                         int32_t* cam_ids /*[CC]*/, int32_t* obs_pt_local /*[l]*/,
+                         int32_t* obs_cam_local /*[l]*/);
+void dbag_partition_destroy(dbag_partition_result* r);
+
 typedef struct dbag_bal dbag_bal;
 int dbag_parse_problem_text(const char* text, size_t len, dbag_bal** out, int32_t* m,
                             int32_t* n, int64_t* l);

@@ -392,6 +392,21 @@ class AdmmSolver:
     def set_copies(self, lp, lc, r, s):
         lib().orc_admm_set_copies(self.h, _p(_f64(lp)), _p(_f64(lc)), _p(_f64(r)), _p(_f64(s)))
 
+    def num_copies(self):
+        pc, cc = C.c_longlong(), C.c_longlong()
+        lib().orc_admm_num_copies(self.h, C.byref(pc), C.byref(cc))
+        return pc.value, cc.value
+
+    def copies_flat(self):
+        """Copies of any BlockConfig, block by block in id order."""
+        pc, cc = self.num_copies()
+        lp, lc, r, s = np.zeros((pc, 3)), np.zeros((cc, 6)), np.zeros((pc, 3)), np.zeros((cc, 6))
+        lib().orc_admm_copies_flat(self.h, _p(lp), _p(lc), _p(r), _p(s), 0)
+        return lp, lc, r, s
+
+    def set_copies_flat(self, lp, lc, r, s):
+        lib().orc_admm_copies_flat(self.h, _p(_f64(lp)), _p(_f64(lc)), _p(_f64(r)), _p(_f64(s)), 1)
+
     def block_obs_ids(self):
         nb = self.nblocks
         np_, nc, no = (np.zeros(nb, np.int32) for _ in range(3))

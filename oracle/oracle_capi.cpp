@@ -518,6 +518,43 @@ void orc_admm_set_copies(void* h, const double* lp, const double* lc, const doub
     }
   }
 }
+// Copies of any BlockConfig, flattened block by block in id order ([PC][3],
+// [CC][6], [PC][3], [CC][6]); dir 0 reads, 1 writes.
+void orc_admm_num_copies(void* h, long long* pc, long long* cc) {
+  long long a = 0, c = 0;
+  for (const LocalBlock& b : S(h).blocks()) {
+    a += (long long)b.point_ids.size();
+    c += (long long)b.cam_ids.size();
+  }
+  *pc = a;
+  *cc = c;
+}
+void orc_admm_copies_flat(void* h, double* lp, double* lc, double* r, double* s, int dir) {
+  AdmmState& st = S(h).state();
+  size_t a = 0, c = 0;
+  for (size_t b = 0; b < st.local_points.size(); ++b) {
+    for (size_t q = 0; q < st.local_points[b].size(); ++q, ++a)
+      for (int k = 0; k < 3; ++k) {
+        if (dir == 0) {
+          lp[3 * a + k] = st.local_points[b][q][k];
+          r[3 * a + k] = st.dual_r[b][q][k];
+        } else {
+          st.local_points[b][q][k] = lp[3 * a + k];
+          st.dual_r[b][q][k] = r[3 * a + k];
+        }
+      }
+    for (size_t q = 0; q < st.local_cameras[b].size(); ++q, ++c)
+      for (int k = 0; k < 6; ++k) {
+        if (dir == 0) {
+          lc[6 * c + k] = st.local_cameras[b][q][k];
+          s[6 * c + k] = st.dual_s[b][q][k];
+        } else {
+          st.local_cameras[b][q][k] = lc[6 * c + k];
+          st.dual_s[b][q][k] = s[6 * c + k];
+        }
+      }
+  }
+}
 // Block structure: counts per block then flattened ids.
 void orc_admm_block_sizes(void* h, int* np, int* nc, int* no) {
   const auto& bl = S(h).blocks();

@@ -103,6 +103,12 @@ SIGNATURES = {
     "dbag_iteration": (C.c_int32, [H]),
     "dbag_num_blocks": (C.c_int64, [H]),
     "dbag_get_block_order": (C.c_int, [H, I32P]),
+    "dbag_num_copies": (C.c_int, [H, I64P, I64P]),
+    "dbag_get_blocks": (C.c_int, [H, I64P, I64P, I32P, I64P, I32P, I32P, I32P]),
+    "dbag_partition": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int32, C.POINTER(H),
+                                 I64P, I64P, I64P, I64P]),
+    "dbag_partition_fetch": (C.c_int, [H, I64P, I32P, I64P, I32P, I64P, I32P, I32P, I32P]),
+    "dbag_partition_destroy": (None, [H]),
     "dbag_max_primal": (C.c_int, [H, DPTR, DPTR]),
     "dbag_dual_sums": (C.c_int, [H, DPTR, DPTR]),
     "dbag_block_objective": (C.c_int, [H, C.c_int64, DPTR]),

@@ -228,8 +228,64 @@ class AdmmOptions:
 
 
 @dataclass
+class LocalBlock:
+    """admm_solver.hpp:35-45: one local subproblem (ids ascending, local indices
+    are positions in point_ids / cam_ids)."""
+    point_ids: np.ndarray
+    cam_ids: np.ndarray
+    obs_ids: np.ndarray
+    obs_point_local: np.ndarray
+    obs_cam_local: np.ndarray
+
+
+def _split_blocks(obs_off, obs_ids, pt_off, pt_ids, cam_off, cam_ids, opl, ocl):
+    out = []
+    for b in range(len(obs_off) - 1):
+        o0, o1 = obs_off[b], obs_off[b + 1]
+        out.append(LocalBlock(pt_ids[pt_off[b]:pt_off[b + 1]].copy(),
+                              cam_ids[cam_off[b]:cam_off[b + 1]].copy(), obs_ids[o0:o1].copy(),
+                              opl[o0:o1].copy(), ocl[o0:o1].copy()))
+    return out
+
+
+def _i64p(a):
+    return a.ctypes.data_as(_capi.I64P)
+
+
+def _partition_arrays(problem, points_per_block, cameras_per_block):
+    lib = _capi.load()
+    h = C.c_void_p()
+    nb, pc, cc, comm = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    pv = problem._view()
+    _check(lib.dbag_partition(C.byref(pv), points_per_block, cameras_per_block, C.byref(h),
+                              C.byref(nb), C.byref(pc), C.byref(cc), C.byref(comm)))
+    try:
+        L = problem.num_observations
+        obs_off, pt_off, cam_off = (np.zeros(nb.value + 1, np.int64) for _ in range(3))
+        obs_ids, opl, ocl = (np.zeros(L, np.int32) for _ in range(3))
+        pt_ids, cam_ids = np.zeros(pc.value, np.int32), np.zeros(cc.value, np.int32)
+        _check(lib.dbag_partition_fetch(h, _i64p(obs_off), _ip(obs_ids), _i64p(pt_off), _ip(pt_ids),
+                                        _i64p(cam_off), _ip(cam_ids), _ip(opl), _ip(ocl)))
+    finally:
+        lib.dbag_partition_destroy(h)
+    return (obs_off, obs_ids, pt_off, pt_ids, cam_off, cam_ids, opl, ocl), comm.value
+
+
+def partition(problem, points_per_block=1, cameras_per_block=1):
+    """partition() (admm_solver.hpp:47, admm_solver.cpp:14-72): list of LocalBlock."""
+    arrays, _ = _partition_arrays(problem, points_per_block, cameras_per_block)
+    return _split_blocks(*arrays)
+
+
+def communication_cost(problem, points_per_block=1, cameras_per_block=1):
+    """communication_cost() (admm_solver.hpp:54, admm_solver.cpp:74-101)."""
+    return _partition_arrays(problem, points_per_block, cameras_per_block)[1]
+
+
+@dataclass
 class AdmmState:
-    """admm_solver.hpp:57-64 for (1,1) blocks, per-copy arrays in block order."""
+    """admm_solver.hpp:57-64, per-copy arrays flattened block by block (in each
+    block's id order); for (1,1) blocks one row per block in block order."""
     local_points: np.ndarray
     local_cameras: np.ndarray
     dual_r: np.ndarray
@@ -344,9 +400,15 @@ class AdmmSolver:
         pose, pts = _f64(state.cam_pose, (-1, 6)), _f64(state.points, (-1, 3))
         _check(self._lib.dbag_set_consensus(self._h, _dp(pose), _dp(pts)))
 
+    def num_copies(self):
+        pc, cc = C.c_int64(), C.c_int64()
+        _check(self._lib.dbag_num_copies(self._h, C.byref(pc), C.byref(cc)))
+        return pc.value, cc.value
+
     def state(self) -> AdmmState:
-        lp, lc = np.zeros((self.l, 3)), np.zeros((self.l, 6))
-        r, s = np.zeros((self.l, 3)), np.zeros((self.l, 6))
+        pc, cc = self.num_copies()
+        lp, lc = np.zeros((pc, 3)), np.zeros((cc, 6))
+        r, s = np.zeros((pc, 3)), np.zeros((cc, 6))
         _check(self._lib.dbag_get_copies(self._h, _dp(lp), _dp(lc), _dp(r), _dp(s)))
         return AdmmState(lp, lc, r, s, self.consensus(), self.iteration)
 
@@ -356,10 +418,22 @@ class AdmmSolver:
         _check(self._lib.dbag_set_copies(self._h, _dp(a), _dp(b), _dp(c), _dp(d)))
 
     def blocks(self):
-        """Block order: blocks()[b].obs_ids[0] for (1,1) blocks."""
+        """Observation ids of all blocks concatenated in block order (for (1,1)
+        blocks: blocks()[b].obs_ids[0])."""
         out = np.zeros(self.l, np.int32)
         _check(self._lib.dbag_get_block_order(self._h, _ip(out)))
         return out
+
+    def block_list(self):
+        """blocks() (admm_solver.hpp:108) as LocalBlock objects."""
+        nb = self._lib.dbag_num_blocks(self._h)
+        pc, cc = self.num_copies()
+        obs_off, pt_off, cam_off = (np.zeros(nb + 1, np.int64) for _ in range(3))
+        pt_ids, cam_ids = np.zeros(pc, np.int32), np.zeros(cc, np.int32)
+        opl, ocl = np.zeros(self.l, np.int32), np.zeros(self.l, np.int32)
+        _check(self._lib.dbag_get_blocks(self._h, _i64p(obs_off), _i64p(pt_off), _ip(pt_ids),
+                                         _i64p(cam_off), _ip(cam_ids), _ip(opl), _ip(ocl)))
+        return _split_blocks(obs_off, self.blocks(), pt_off, pt_ids, cam_off, cam_ids, opl, ocl)
 
     # ---- queries (admm_solver.hpp:110-127)
     def max_primal_residual_points(self):

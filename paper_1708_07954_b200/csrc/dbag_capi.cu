@@ -2,18 +2,21 @@
 // build, round orchestration on one stream, queries. Compiled for sm_100a only.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
 #include <array>
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/dbag.h"
 #include "dbag_common.cuh"
 #include "dbag_consensus.cuh"
+#include "dbag_blocks.h"
 #include "dbag_exact.h"
 #include "dbag_shard.h"
 #include <nccl.h>
@@ -112,6 +115,9 @@ struct dbag_solver {
   std::vector<int32_t> local_points;  // local -> global point id (sharded only)
   ncclComm_t comm = nullptr;
   bool sharded() const { return world > 1; }
+  // generalized blocks (BlockConfig != {1,1}); null for (1,1)
+  std::unique_ptr<blocks::GenSolver> gen;
+  int64_t num_blocks() const { return gen ? gen->G.B : S.L; }
 
   ~dbag_solver() {
     cudaSetDevice(device);
@@ -129,6 +135,10 @@ struct dbag_solver {
   bool exact() const { return opts.numerics == DBAG_NUMERICS_EXACT; }
 
   void launch_camera(int mode) {
+    if (gen) {
+      CK(gen->cameras(S, mode, stream));
+      return;
+    }
     if (exact()) {
       CK(exact::launch_camera(S, mode, stream));
       return;
@@ -143,6 +153,10 @@ struct dbag_solver {
   }
 
   void launch_point(int mode, bool metric) {
+    if (gen) {
+      CK(gen->points(S, mode, metric, n_pt_parts, stream));
+      return;
+    }
     if (exact()) {
       CK(exact::launch_point(S, mode, metric, n_pt_parts, stream));
       return;
@@ -168,6 +182,10 @@ struct dbag_solver {
   }
 
   void launch_local(int64_t begin, int64_t count) {
+    if (gen) {
+      CK(gen->local(S, begin, count, stream));
+      return;
+    }
     if (exact()) {
       CK(exact::launch_local(S, begin, count, stream));
       return;
@@ -200,7 +218,7 @@ struct dbag_solver {
   void phase0(cudaEvent_t* e) {
     reset_err();
     CK(cudaEventRecord(e[0], stream));
-    launch_local(0, S.L);
+    launch_local(0, num_blocks());
     CK(cudaEventRecord(e[1], stream));
     launch_camera(kModeConsensus | kModeDual);
     if (sharded() && S.send_count > 0) {
@@ -619,9 +637,17 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
       raise(DBAG_ERR_VALIDATION, "numerics must be FAST (0) or EXACT (1)");
     if (o.points_per_block < 1 || o.cameras_per_block < 1)
       raise(DBAG_ERR_VALIDATION, "block sizes must be >= 1");
-    if (o.points_per_block != 1 || o.cameras_per_block != 1)
-      raise(DBAG_ERR_UNSUPPORTED, "only (1,1) blocks are built on the device (SURVEY §8(f) row 1)");
     h->L_total = L;
+    if (o.points_per_block != 1 || o.cameras_per_block != 1) {
+      // generalized blocks: partition over the K0 (cam, pt) order, copies, maps
+      h->gen = std::make_unique<blocks::GenSolver>();
+      const cudaError_t e = h->gen->init(h->S, o.points_per_block, o.cameras_per_block, h->device, st);
+      if (e == cudaErrorInvalidConfiguration)
+        raise(DBAG_ERR_UNSUPPORTED, "block too large for one CTA's shared memory");
+      CK(e);
+      CK(cudaStreamSynchronize(st));
+      h->comm_floats = h->gen->comm_floats;
+    }
     h->M_total = M;
     h->N_total = N;
   }
@@ -647,6 +673,8 @@ int dbag_create_sharded(const dbag_problem_view* F, const dbag_param_view* init,
   auto* h = new dbag_solver();
   const int rc = guarded([&] {
     if (world < 1 || rank < 0 || rank >= world) raise(DBAG_ERR_VALIDATION, "bad rank/world");
+    if (opts->points_per_block != 1 || opts->cameras_per_block != 1)
+      raise(DBAG_ERR_UNSUPPORTED, "sharded solves use (1,1) blocks");
     if (init->num_cameras != F->num_cameras || init->num_points != F->num_points)
       raise(DBAG_ERR_SIZE_MISMATCH, "init state sizes do not match the problem");
     ShardPlan plan;
@@ -810,7 +838,7 @@ void dbag_destroy(dbag_solver* h) { delete h; }
 
 int dbag_local_update(dbag_solver* h, int64_t block) {
   return guarded([&] {
-    if (block < 0 || block >= h->S.L) raise(DBAG_ERR_VALIDATION, "block index out of range");
+    if (block < 0 || block >= h->num_blocks()) raise(DBAG_ERR_VALIDATION, "block index out of range");
     CK(cudaSetDevice(h->device));
     h->reset_err();
     h->launch_local(block, 1);
@@ -823,7 +851,7 @@ int dbag_local_update_all(dbag_solver* h) {
   return guarded([&] {
     CK(cudaSetDevice(h->device));
     h->reset_err();
-    h->launch_local(0, h->S.L);
+    h->launch_local(0, h->num_blocks());
     h->sync();
     h->check_local_error();
   });
@@ -947,6 +975,10 @@ int dbag_set_consensus(dbag_solver* h, const double* cam_pose, const double* poi
 static int copies_io(dbag_solver* h, double* lp, double* lc, double* r, double* s, int dir) {
   return guarded([&] {
     CK(cudaSetDevice(h->device));
+    if (h->gen) {
+      CK(h->gen->copies_io(lp, lc, r, s, dir, h->stream));
+      return;
+    }
     const int64_t L = h->S.L;
     double* d = nullptr;
     CK(cudaMalloc(&d, sizeof(double) * 18 * L));
@@ -979,8 +1011,110 @@ int dbag_set_copies(dbag_solver* h, const double* lp, const double* lc, const do
                    const_cast<double*>(s), 1);
 }
 
+// ---- host-only partition() / communication_cost() (admm_solver.cpp:14-101)
+struct dbag_partition_result {
+  blocks::Partition P;
+  std::vector<int32_t> obs_ids;  // block order (sorted by (cam_id, point_id))
+};
+
+int dbag_partition(const dbag_problem_view* p, int32_t points_per_block, int32_t cameras_per_block,
+                   dbag_partition_result** out, int64_t* n_blocks, int64_t* n_point_copies,
+                   int64_t* n_cam_copies, int64_t* comm_floats) {
+  *out = nullptr;
+  auto* r = new dbag_partition_result();
+  const int rc = guarded([&] {
+    if (points_per_block < 1 || cameras_per_block < 1)
+      raise(DBAG_ERR_VALIDATION, "block sizes must be >= 1");
+    const int64_t L = p->num_obs;
+    for (int64_t k = 0; k < L; ++k)
+      if (p->obs_cam[k] < 0 || p->obs_cam[k] >= p->num_cameras || p->obs_pt[k] < 0 ||
+          p->obs_pt[k] >= p->num_points)
+        raise(DBAG_ERR_INDEX_OUT_OF_RANGE, "observation " + std::to_string(k) + " index out of range");
+    r->obs_ids.resize(L);
+    for (int64_t k = 0; k < L; ++k) r->obs_ids[k] = (int32_t)k;
+    std::stable_sort(r->obs_ids.begin(), r->obs_ids.end(), [&](int32_t a, int32_t b) {
+      return std::make_pair(p->obs_cam[a], p->obs_pt[a]) < std::make_pair(p->obs_cam[b], p->obs_pt[b]);
+    });
+    std::vector<int32_t> cam(L), pt(L);
+    for (int64_t k = 0; k < L; ++k) {
+      cam[k] = p->obs_cam[r->obs_ids[k]];
+      pt[k] = p->obs_pt[r->obs_ids[k]];
+    }
+    r->P = blocks::partition_sorted(L, cam.data(), pt.data(), points_per_block, cameras_per_block);
+    if (n_blocks) *n_blocks = r->P.blocks();
+    if (n_point_copies) *n_point_copies = (int64_t)r->P.pt_ids.size();
+    if (n_cam_copies) *n_cam_copies = (int64_t)r->P.cam_ids.size();
+    if (comm_floats) *comm_floats = blocks::communication_cost(r->P, p->num_cameras, p->num_points);
+  });
+  if (rc != DBAG_OK) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return DBAG_OK;
+}
+
+int dbag_partition_fetch(const dbag_partition_result* r, int64_t* obs_off, int32_t* obs_ids,
+                         int64_t* pt_off, int32_t* pt_ids, int64_t* cam_off, int32_t* cam_ids,
+                         int32_t* obs_pt_local, int32_t* obs_cam_local) {
+  return guarded([&] {
+    auto put = [](auto* dst, const auto& v) {
+      if (dst) std::copy(v.begin(), v.end(), dst);
+    };
+    put(obs_off, r->P.obs_off);
+    put(obs_ids, r->obs_ids);
+    put(pt_off, r->P.pt_off);
+    put(pt_ids, r->P.pt_ids);
+    put(cam_off, r->P.cam_off);
+    put(cam_ids, r->P.cam_ids);
+    put(obs_pt_local, r->P.obs_pl);
+    put(obs_cam_local, r->P.obs_cl);
+  });
+}
+
+void dbag_partition_destroy(dbag_partition_result* r) { delete r; }
+
 int32_t dbag_iteration(dbag_solver* h) { return h->iteration; }
-int64_t dbag_num_blocks(dbag_solver* h) { return h->S.L; }
+int64_t dbag_num_blocks(dbag_solver* h) { return h->num_blocks(); }
+
+int dbag_num_copies(dbag_solver* h, int64_t* point_copies, int64_t* cam_copies) {
+  return guarded([&] {
+    if (point_copies) *point_copies = h->gen ? h->gen->G.PC : h->S.L;
+    if (cam_copies) *cam_copies = h->gen ? h->gen->G.CC : h->S.L;
+  });
+}
+
+int dbag_get_blocks(dbag_solver* h, int64_t* obs_off, int64_t* pt_off, int32_t* pt_ids,
+                    int64_t* cam_off, int32_t* cam_ids, int32_t* obs_pt_local,
+                    int32_t* obs_cam_local) {
+  return guarded([&] {
+    CK(cudaSetDevice(h->device));
+    const int64_t L = h->S.L;
+    if (h->gen) {
+      const blocks::Partition& P = h->gen->part;
+      auto put = [](auto* dst, const auto& v) {
+        if (dst) std::copy(v.begin(), v.end(), dst);
+      };
+      put(obs_off, P.obs_off);
+      put(pt_off, P.pt_off);
+      put(pt_ids, P.pt_ids);
+      put(cam_off, P.cam_off);
+      put(cam_ids, P.cam_ids);
+      put(obs_pt_local, P.obs_pl);
+      put(obs_cam_local, P.obs_cl);
+      return;
+    }
+    for (int64_t b = 0; b <= L; ++b) {  // (1,1): block b = sorted observation b
+      if (obs_off) obs_off[b] = b;
+      if (pt_off) pt_off[b] = b;
+      if (cam_off) cam_off[b] = b;
+    }
+    if (pt_ids) CK(cudaMemcpy(pt_ids, h->S.blk_pt, 4 * L, cudaMemcpyDeviceToHost));
+    if (cam_ids) CK(cudaMemcpy(cam_ids, h->S.blk_cam, 4 * L, cudaMemcpyDeviceToHost));
+    if (obs_pt_local) std::fill(obs_pt_local, obs_pt_local + L, 0);
+    if (obs_cam_local) std::fill(obs_cam_local, obs_cam_local + L, 0);
+  });
+}
 
 int dbag_get_block_order(dbag_solver* h, int32_t* obs_ids) {
   return guarded([&] {
@@ -992,6 +1126,16 @@ int dbag_get_block_order(dbag_solver* h, int32_t* obs_ids) {
 int dbag_max_primal(dbag_solver* h, double* max_x, double* max_y) {
   return guarded([&] {
     CK(cudaSetDevice(h->device));
+    if (h->gen) {
+      double* d = h->S.record + kRecFields;
+      CK(h->gen->max_primal(h->S, d, h->stream));
+      double o[2];
+      CK(cudaMemcpyAsync(o, d, sizeof(o), cudaMemcpyDeviceToHost, h->stream));
+      h->sync();
+      *max_x = o[0];
+      *max_y = o[1];
+      return;
+    }
     // primal-only pass: camera and point kernels in dual mode on a scratch copy
     // would mutate duals; instead evaluate directly.
     const DevState& S = h->S;
@@ -1029,8 +1173,12 @@ int dbag_dual_sums(dbag_solver* h, double* point_sums, double* cam_sums) {
     const DevState& S = h->S;
     double* d = nullptr;
     CK(cudaMalloc(&d, sizeof(double) * (3 * (size_t)S.N + 6 * (size_t)S.M + 1)));
-    k_dual_sums<<<grid_for((int64_t)S.N + S.M, 128), 128, 0, h->stream>>>(S, d, d + 3 * (size_t)S.N);
-    CK_LAUNCH();
+    if (h->gen) {
+      CK(h->gen->dual_sums(S, d, d + 3 * (size_t)S.N, h->stream));
+    } else {
+      k_dual_sums<<<grid_for((int64_t)S.N + S.M, 128), 128, 0, h->stream>>>(S, d, d + 3 * (size_t)S.N);
+      CK_LAUNCH();
+    }
     CK(cudaMemcpyAsync(point_sums, d, sizeof(double) * 3 * S.N, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaMemcpyAsync(cam_sums, d + 3 * (size_t)S.N, sizeof(double) * 6 * S.M,
                        cudaMemcpyDeviceToHost, h->stream));
@@ -1041,17 +1189,23 @@ int dbag_dual_sums(dbag_solver* h, double* point_sums, double* cam_sums) {
 
 int dbag_block_objective(dbag_solver* h, int64_t block, double* out) {
   return guarded([&] {
-    if (block < 0 || block >= h->S.L) raise(DBAG_ERR_VALIDATION, "block index out of range");
+    if (block < 0 || block >= h->num_blocks()) raise(DBAG_ERR_VALIDATION, "block index out of range");
     CK(cudaSetDevice(h->device));
-    k_block_objective<<<1, 1, 0, h->stream>>>(h->S, block, h->S.record + kRecFields);
-    CK_LAUNCH();
+    if (h->gen) {
+      CK(h->gen->block_objective(h->S, block, h->S.record + kRecFields, h->stream));
+    } else {
+      k_block_objective<<<1, 1, 0, h->stream>>>(h->S, block, h->S.record + kRecFields);
+      CK_LAUNCH();
+    }
     CK(cudaMemcpyAsync(out, h->S.record + kRecFields, sizeof(double), cudaMemcpyDeviceToHost,
                        h->stream));
     h->sync();
   });
 }
 
-int64_t dbag_ops_per_iteration(dbag_solver* h) { return 3 * h->L_total; }  // blocks + 2 copies each
+int64_t dbag_ops_per_iteration(dbag_solver* h) {  // blocks + copies (admm_solver.cpp:428-435)
+  return h->gen ? h->gen->ops_per_iteration() : 3 * h->L_total;
+}
 int64_t dbag_comm_floats(dbag_solver* h) { return h->comm_floats; }
 
 int dbag_mean_reprojection_error(dbag_solver* h, double* out) {
@@ -1077,6 +1231,7 @@ int dbag_reset(dbag_solver* h) {
     k_reset_consensus<<<grid_for(std::max(S.M, S.N), 256), 256, 0, h->stream>>>(S, h->init_pose,
                                                                                 h->init_pts);
     CK_LAUNCH();
+    if (h->gen) CK(h->gen->reset_copies(S, h->stream));
     h->sync();
     h->iteration = 0;
   });

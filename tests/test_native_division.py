@@ -1,7 +1,8 @@
-"""The EXACT kernels replace IEEE division by a shared correctly rounded
-reciprocal plus Markstein's correction (dbag_exact.cu qdiv/qdiv_run). This
-fuzz checks bit-identity with '/' (including the sign of zero) on random,
-adversarial and LDLT-like operands, compiled with hardware FMA."""
+"""Markstein division (a shared correctly rounded reciprocal plus one FMA
+correction) against IEEE '/': the identity behind the shared-reciprocal LDLT
+variants recorded in DESIGN.md §4 (bit-identical, measured slower, not
+shipped). This fuzz checks bit-identity with '/' (including the sign of zero)
+on random, adversarial and LDLT-like operands, compiled with hardware FMA."""
 import os
 import subprocess
 
