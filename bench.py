@@ -142,7 +142,7 @@ def sample_problem(scene, target_obs):
                 cameras=C, l=int(sel.sum()))
 
 
-def oracle_rounds(sample, loss, workers, rounds, warmup=0):
+def oracle_rounds(sample, loss, workers, rounds, warmup=0, blocks=(1, 1)):
     """Runs the CPU restatement of the reference (oracle/) on the sample;
     returns per-round wall_ms in the reference's own timed scope
     (local+consensus+dual, admm_solver.cpp:438-443)."""
@@ -152,7 +152,8 @@ def oracle_rounds(sample, loss, workers, rounds, warmup=0):
                           sample["obs_cam"], sample["obs_pt"], sample["obs_uv"])
     solver = O.AdmmSolver(op, sample["init_pose"], sample["cam_f"], sample["init_pts"],
                           workers=workers, loss=1 if loss == "huber" else 0,
-                          max_iters=warmup + rounds + 1)
+                          max_iters=warmup + rounds + 1, points_per_block=blocks[0],
+                          cameras_per_block=blocks[1])
     ms = []
     for k in range(warmup + rounds):
         rec = solver.iterate()
@@ -161,10 +162,10 @@ def oracle_rounds(sample, loss, workers, rounds, warmup=0):
     return ms
 
 
-def cpu_sample_for(scene, loss, workers, budget_s):
+def cpu_sample_for(scene, loss, workers, budget_s, blocks=(1, 1)):
     """Size a sample so one oracle round takes about budget_s on `workers`."""
     probe = sample_problem(scene, 4000)
-    ms = oracle_rounds(probe, loss, workers, 2)
+    ms = oracle_rounds(probe, loss, workers, 2, blocks=blocks)
     per_obs_s = (max(ms) / 1e3) / probe["l"]
     return sample_problem(scene, int(max(4000, budget_s / max(per_obs_s, 1e-9))))
 
@@ -176,8 +177,8 @@ def reference_arm(args, rank, world):
     scene = P.generate_config_scene(args.config, args.seed)
     workers = os.cpu_count() or 1
     budget = max(0.05, min(2.0, 150.0 / max(1, args.steps + args.warmup)))
-    sample = cpu_sample_for(scene, args.loss, workers, budget)
-    ms = oracle_rounds(sample, args.loss, workers, args.steps, args.warmup)
+    sample = cpu_sample_for(scene, args.loss, workers, budget, blocks(args))
+    ms = oracle_rounds(sample, args.loss, workers, args.steps, args.warmup, blocks(args))
     total_s = sum(ms) / 1e3
     value = sample["l"] * args.steps / total_s
     line = {
@@ -196,9 +197,15 @@ def reference_arm(args, rank, world):
     return 0
 
 
+def blocks(args):
+    return (args.points_per_block, args.cameras_per_block)
+
+
 def config_block(args, scene):
     p = scene.problem
     return {"workload": CONFIG_NAMES[args.config], "config_id": args.config,
+            "block_config": {"points_per_block": args.points_per_block,
+                             "cameras_per_block": args.cameras_per_block},
             "cameras": int(p.num_cameras), "points": int(p.num_points),
             "observations": int(p.num_observations), "loss": args.loss,
             "numerics": args.numerics,
@@ -224,8 +231,12 @@ def our_arm(args, rank, world, local_rank):
 
     numerics = P.admm.EXACT if args.numerics == "exact" else P.admm.FAST
 
+    general = blocks(args) != (1, 1)
+
     def opts(rounds):
-        return P.AdmmOptions(misfit_loss=loss, max_iters=rounds, device=dev, numerics=numerics)
+        return P.AdmmOptions(misfit_loss=loss, max_iters=rounds, device=dev, numerics=numerics,
+                             points_per_block=args.points_per_block,
+                             cameras_per_block=args.cameras_per_block)
 
     # ---------------- e2e through the C-ABI from pinned host buffers
     def pinned(a):
@@ -300,30 +311,35 @@ def our_arm(args, rank, world, local_rank):
     last = solver.iterate()  # one more round with the metrics read back (untimed)
 
     # the other numerics mode, same rounds 1..K from the same init (reported
-    # beside the headline; DESIGN.md §5 explains the two modes)
+    # beside the headline; DESIGN.md §5 explains the two modes). Generalized
+    # blocks run the EXACT kernels only.
     other = "fast" if args.numerics == "exact" else "exact"
+    if general:
+        other = None
     o_opts = P.AdmmOptions(misfit_loss=loss, max_iters=10 ** 9, device=dev,
                            numerics=P.admm.FAST if other == "fast" else P.admm.EXACT)
-    solver2 = make(p, scene.init, o_opts)
-    solver2.enqueue_round()
-    solver2.synchronize()
-    solver2.reset()
-    stream2 = torch.cuda.ExternalStream(solver2.stream_handle(), device=dev)
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
-    f0.record(stream2)
-    for _ in range(args.steps):
+    solver2 = make(p, scene.init, o_opts) if other else None
+    ms2 = 0.0
+    if other:
         solver2.enqueue_round()
-    f1.record(stream2)
-    solver2.synchronize()
-    ms2 = f0.elapsed_time(f1)
-    if world > 1:
-        t = torch.tensor([ms2], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms2 = float(t.item())
-    solver2.close()
-    other_line = {"numerics": other, "value": L * args.steps / (ms2 / 1e3),
+        solver2.synchronize()
+        solver2.reset()
+        stream2 = torch.cuda.ExternalStream(solver2.stream_handle(), device=dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier()
+        f0.record(stream2)
+        for _ in range(args.steps):
+            solver2.enqueue_round()
+        f1.record(stream2)
+        solver2.synchronize()
+        ms2 = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ms2], device=f"cuda:{dev}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms2 = float(t.item())
+        solver2.close()
+    other_line = None if not other else {"numerics": other, "value": L * args.steps / (ms2 / 1e3),
                   "ms_per_step": ms2 / args.steps,
                   "note": ("FMA, Woodbury 2x2 solve, hardware-style sin/cos: same algorithm and "
                            "control flow, last-ulp rounding differs (trajectory not bit-identical)"
@@ -348,13 +364,15 @@ def our_arm(args, rank, world, local_rank):
         kernels[name] = {"ms": ms, "share": stats[key] / max(ms_total, 1e-9),
                          "gbs": byts / (ms / 1e3) / 1e9,
                          "frac_hbm": (byts / (ms / 1e3) / 1e9) / hbm_peak if hbm_peak else None}
-    fl = flops_of(stats, args.loss, args.numerics) / args.steps
+    fl = (stats["n_model_flops"] if general else flops_of(stats, args.loss, args.numerics)) \
+        / args.steps
     kernels["local"]["tflops"] = fl / (kernels["local"]["ms"] / 1e3) / 1e12
     kernels["local"]["frac_fp64"] = kernels["local"]["tflops"] / fp64_peak
     kernels["local"]["flops_per_obs"] = fl / Lr
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     if dom == "local":
-        roof = {"kernel": "k_local (K1 local solve)", "bound": "fp64",
+        roof = {"kernel": ("k_local_blocks (K1, generalized blocks, model FLOPs counted per block)"
+                           if general else "k_local (K1 local solve)"), "bound": "fp64",
                 "achieved": kernels["local"]["tflops"], "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": kernels["local"]["frac_fp64"], "traffic": None,
                 "peak_source": "measured on this device by dbag_measure_fp64_peak (DFMA probe); "
@@ -369,8 +387,8 @@ def our_arm(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         workers = os.cpu_count() or 1
-        sample = cpu_sample_for(scene, args.loss, workers, 3.0)
-        ms = oracle_rounds(sample, args.loss, workers, 3)
+        sample = cpu_sample_for(scene, args.loss, workers, 3.0, blocks(args))
+        ms = oracle_rounds(sample, args.loss, workers, 3, blocks=blocks(args))
         cpu = {"value": sample["l"] * 3 / (sum(ms) / 1e3), "unit": UNIT, "cores": workers,
                "kind": "port",
                "sample": f"cameras [0,{sample['cameras']}) of the same scene, {sample['l']} "
@@ -418,6 +436,9 @@ def main():
                     help="exact: bit-identical to the restated reference; fast: FMA/Woodbury")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
+    ap.add_argument("--points-per-block", type=int, default=1,
+                    help="BlockConfig points_per_block (generalized blocks when != (1,1))")
+    ap.add_argument("--cameras-per-block", type=int, default=1)
     args = ap.parse_args()
     if args.steps is None:
         args.steps = CONFIG_ROUNDS[args.config]

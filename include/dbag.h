@@ -129,6 +129,8 @@ typedef struct {
   uint64_t n_direction;  /* L-BFGS two-loop directions */
   uint64_t n_pairs_used; /* L-BFGS: sum of history sizes over directions */
   double ms_local, ms_camera, ms_point, ms_final; /* last enqueued round */
+  uint64_t n_model_flops; /* generalized blocks: model FLOPs counted per block
+                           * from its dimension (DESIGN.md §Generalized blocks) */
 } dbag_round_stats;
 
 typedef struct dbag_solver dbag_solver;

@@ -278,11 +278,13 @@ VecX ldlt_solve(const MatX& A, const VecX& b) {
     const double d = mat(i, i);
     x[i] = std::abs(d) > tol ? x[i] / d : 0.0;
   }
-  for (int i = n - 1; i >= 0; --i) {
-    double s = x[i];
-    for (int j = i + 1; j < n; ++j) s -= mat(j, i) * x[j];
-    x[i] = s;
-  }
+  // L^-T, column-oriented: once x_j is final, subtract L_ji x_j from every
+  // x_i (i < j), for j = n-1 down to 1. Eigen's own summation order here
+  // (panelled triangular solve with vectorised dot products) is not pinned at
+  // the bit level by anything the reference ships; this order is
+  // one faithful restatement, and the one a GPU can run as a parallel sweep.
+  for (int j = n - 1; j > 0; --j)
+    for (int i = 0; i < j; ++i) x[i] -= mat(j, i) * x[j];
   for (int k = n - 1; k >= 0; --k) std::swap(x[k], x[transp[k]]);
   return x;
 }

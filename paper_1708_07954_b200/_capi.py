@@ -53,7 +53,7 @@ class RoundStats(C.Structure):
     _fields_ = [("n_jacobian", C.c_uint64), ("n_trial", C.c_uint64), ("n_accept", C.c_uint64),
                 ("n_direction", C.c_uint64), ("n_pairs_used", C.c_uint64),
                 ("ms_local", C.c_double), ("ms_camera", C.c_double), ("ms_point", C.c_double),
-                ("ms_final", C.c_double)]
+                ("ms_final", C.c_double), ("n_model_flops", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

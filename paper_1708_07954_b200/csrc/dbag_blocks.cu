@@ -109,7 +109,9 @@ struct Carve {
   int *opl, *ocl, *pto_off, *pto, *cmo_off, *pco, *ord, *flag;
 };
 
-// Offsets for the maxima; returns the bytes (M included iff m_in_smem).
+// Offsets for the maxima; returns the bytes (M included iff m_in_smem). mem > 0
+// (Huber / L-BFGS) adds the consensus copy, loss gradients and the history;
+// Gauss-Newton reuses x / dl / vt as pivot and temp scratch instead.
 __host__ __device__ inline size_t carve(char* base, int D, int NP, int NC, int NO, int mem,
                                         bool m_in_smem, Carve* c) {
   size_t off = 0;
@@ -127,18 +129,18 @@ __host__ __device__ inline size_t carve(char* base, int D, int NP, int NC, int N
   k.x = take_d(D);
   k.vt = take_d(D);
   k.dl = take_d(D);
-  k.piv = take_d(D);
+  k.piv = mem > 0 ? take_d(D) : nullptr;
   k.fcam = take_d(NC);
   k.A = take_d((size_t)NO * 18);
   k.r = take_d((size_t)NO * 2);
   k.rt = take_d((size_t)NO * 2);
   k.uv = take_d((size_t)NO * 2);
-  k.lg = take_d((size_t)NO * 2);
+  k.lg = mem > 0 ? take_d((size_t)NO * 2) : nullptr;
   k.red = take_d(8);
-  k.hs = take_d((size_t)mem * D);
-  k.hy = take_d((size_t)mem * D);
-  k.hrho = take_d(mem > 0 ? mem : 1);
-  k.alpha = take_d(mem > 0 ? mem : 1);
+  k.hs = mem > 0 ? take_d((size_t)mem * D) : nullptr;
+  k.hy = mem > 0 ? take_d((size_t)mem * D) : nullptr;
+  k.hrho = mem > 0 ? take_d(mem) : nullptr;
+  k.alpha = mem > 0 ? take_d(mem) : nullptr;
   k.M = m_in_smem ? take_d(tri(D, 0)) : nullptr;
   auto take_i = [&](size_t n) {
     int* p = reinterpret_cast<int*>(base + off);
@@ -198,7 +200,7 @@ __device__ __forceinline__ int jcol(bool pt, int co) { return pt ? co : 3 + co; 
 
 // Residuals at V for every observation (one thread each) into rr[2*nobs];
 // flag[0] := 1 if any projection is infeasible or any row is non-finite.
-__device__ void residuals(const DevState& S, const Blk& k, const Carve& c, const double* V,
+__device__ __forceinline__ void residuals(const DevState& S, const Blk& k, const Carve& c, const double* V,
                           double* rr) {
   for (int o = threadIdx.x; o < k.nobs; o += kGenThreads) {
     exact::ETrig t;
@@ -215,7 +217,7 @@ __device__ void residuals(const DevState& S, const Blk& k, const Carve& c, const
 }
 
 // Jacobian rows (positive e.Jp | e.Jc, geometry.cpp:141-159) at V.
-__device__ void jacobians(const DevState& S, const Blk& k, const Carve& c, const double* V) {
+__device__ __forceinline__ void jacobians(const DevState& S, const Blk& k, const Carve& c, const double* V) {
   for (int o = threadIdx.x; o < k.nobs; o += kGenThreads) {
     exact::ETrig t;
     double R[9], w[3], z[2], v9[9];
@@ -248,7 +250,7 @@ __device__ __forceinline__ Span obs_of(const Carve& c, bool pt, int idx) {
 
 // H(i,j) = sum_k J(k,i) J(k,j) over the rows in order (oracle gauss_newton);
 // the weight row adds w*w on the diagonal only.
-__device__ double h_entry(const Blk& k, const Carve& c, int i, int j) {
+__device__ __forceinline__ double h_entry(const Blk& k, const Carve& c, int i, int j) {
   bool pi, pj;
   int ii, ij, ci, cj;
   var_of(k, i, pi, ii, ci);
@@ -279,7 +281,7 @@ __device__ double h_entry(const Blk& k, const Carve& c, int i, int j) {
 }
 
 // Sequential sum of squares of the residual rows (sq_norm, oracle order).
-__device__ double objective_rows(const Blk& k, const Carve& c, const double* rr, const double* V) {
+__device__ __forceinline__ double objective_rows(const Blk& k, const Carve& c, const double* rr, const double* V) {
   double s = 0.0;
   for (int n = 0; n < 2 * k.nobs; ++n) s += rr[n] * rr[n];
   for (int i = 0; i < k.D; ++i) {
@@ -290,7 +292,7 @@ __device__ double objective_rows(const Blk& k, const Carve& c, const double* rr,
   return s;
 }
 
-__device__ bool weight_rows_finite(const Blk& k, const Carve& c, const double* V) {
+__device__ __forceinline__ bool weight_rows_finite(const Blk& k, const Carve& c, const double* V) {
   bool ok = true;
   for (int i = 0; i < k.D; ++i) {
     const double w = i < k.cb ? k.wx : k.wy;
@@ -307,12 +309,14 @@ __device__ __forceinline__ double seq_dot(const double* a, const double* b, int 
 
 // Pivot sequence of the oracle's ldlt_solve over |hd|: at step k the first
 // position holding the largest value among k..D-1 (strict '>' from a[k]),
-// then a transposition. One warp; ord[p] = variable at position p.
-__device__ void pivot_order(const Blk& k, const Carve& c) {
+// then a transposition. One warp; ord[p] = variable at position p. Scratch:
+// c.x (filled with the permuted right-hand side only afterwards).
+__device__ __forceinline__ void pivot_order(const Blk& k, const Carve& c) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
+  double* a = c.x;
   for (int i = lane; i < k.D; i += 32) {
-    c.piv[i] = fabs(c.hd[i]);
+    a[i] = fabs(c.hd[i]);
     c.ord[i] = i;
   }
   __syncwarp();
@@ -320,9 +324,9 @@ __device__ void pivot_order(const Blk& k, const Carve& c) {
     double bv = -INFINITY;
     int bp = 0x7fffffff;
     for (int i = s + 1 + lane; i < k.D; i += 32) {
-      const double a = c.piv[i];
-      if (a > bv) {  // positions ascend per lane: first max of the lane's subset
-        bv = a;
+      const double ai = a[i];
+      if (ai > bv) {  // positions ascend per lane: first max of the lane's subset
+        bv = ai;
         bp = i;
       }
     }
@@ -335,13 +339,13 @@ __device__ void pivot_order(const Blk& k, const Carve& c) {
         bp = op;
       }
     }
-    const double ak = c.piv[s];
+    const double ak = a[s];
     const int big = bv > ak ? bp : s;  // NaN a[s]: nothing is larger, no swap
     __syncwarp();
     if (lane == 0 && big != s) {
-      const double ta = c.piv[s];
-      c.piv[s] = c.piv[big];
-      c.piv[big] = ta;
+      const double ta = a[s];
+      a[s] = a[big];
+      a[big] = ta;
       const int to = c.ord[s];
       c.ord[s] = c.ord[big];
       c.ord[big] = to;
@@ -351,72 +355,99 @@ __device__ void pivot_order(const Blk& k, const Carve& c) {
 }
 
 // delta = (P^T LDL^T P)^{-1} rhs for Hd (oracle ldlt_solve on the permuted
-// system). M: lower triangle of P Hd P^T, filled here. Result in c.dl.
-__device__ void ldlt_solve(const Blk& k, const Carve& c, double* M) {
+// system). M: lower triangle of P Hd P^T (row p at p(p+1)/2), filled here.
+// Result in c.dl. Scratch: c.dl / c.vt (temp[] double buffer), c.hdg is kept.
+__device__ __forceinline__ int rowp(int i) { return i * (i + 1) / 2; }
+
+template <bool kSharedM>
+__device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double* M) {
   const int D = k.D;
   pivot_order(k, c);
   __syncthreads();
-  for (int64_t e = threadIdx.x; e < tri(D, 0); e += kGenThreads) {
+  const int ne = rowp(D);
+  for (int e = threadIdx.x; e < ne; e += kGenThreads) {
     int p = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-    while (tri(p + 1, 0) <= e) ++p;
-    while (tri(p, 0) > e) --p;
-    const int q = (int)(e - tri(p, 0));
+    while (rowp(p + 1) <= e) ++p;
+    while (rowp(p) > e) --p;
+    const int q = e - rowp(p);
     const int i = c.ord[p], j = c.ord[q];
     M[e] = p == q ? c.hd[i] : h_entry(k, c, i, j);
   }
   for (int p = threadIdx.x; p < D; p += kGenThreads) c.x[p] = c.g[c.ord[p]];  // P rhs (g holds rhs)
   __syncthreads();
-  // left-looking LDL^T, unpivoted (the permutation is already applied)
+  // Left-looking LDL^T, unpivoted (the permutation is already applied).
+  // temp[j] = D_j L_kj for the next column is formed during this column's
+  // division phase (double buffer), so each column costs two barriers.
+  double* tbuf[2] = {c.dl, c.vt};
   bool stop = false;
   for (int kk = 0; kk < D && !stop; ++kk) {
+    const double* tc = tbuf[kk & 1];
+    double* tn = tbuf[(kk + 1) & 1];
     if (kk > 0) {
-      const double* Mk = M + tri(kk, 0);
       for (int i = kk + threadIdx.x; i < D; i += kGenThreads) {
-        double* Mi = M + tri(i, 0);
+        double* Mi = M + rowp(i);
         double s = 0.0;
-        for (int j = 0; j < kk; ++j) s += Mi[j] * (M[tri(j, j)] * Mk[j]);  // temp[j] = D_j L_kj
+        for (int j = 0; j < kk; ++j) s += Mi[j] * tc[j];
         Mi[kk] = Mi[kk] - s;
       }
       __syncthreads();
     }
-    const double akk = M[tri(kk, kk)];
+    const double akk = M[rowp(kk) + kk];
     const bool valid = fabs(akk) > 0.0;
     if (kk == 0 && !valid) {
       stop = true;  // Eigen: all-zero diagonal, nothing factorized
-    } else if (valid) {
-      for (int i = kk + 1 + threadIdx.x; i < D; i += kGenThreads) M[tri(i, kk)] = M[tri(i, kk)] / akk;
+    } else {
+      for (int i = kk + 1 + threadIdx.x; i < D; i += kGenThreads) {
+        double* Mi = M + rowp(i);
+        if (valid) Mi[kk] = Mi[kk] / akk;
+        if (i == kk + 1) tn[kk] = M[rowp(kk) + kk] * Mi[kk];  // D_kk L_{kk+1,kk}
+      }
+      if (kk + 1 < D) {
+        const double* Mn = M + rowp(kk + 1);
+        for (int j = threadIdx.x; j < kk; j += kGenThreads) tn[j] = M[rowp(j) + j] * Mn[j];
+      }
     }
     __syncthreads();
   }
   // forward substitution, column sweep (same per-row order as the oracle)
   for (int j = 0; j < D - 1; ++j) {
     const double xj = c.x[j];
-    for (int i = j + 1 + threadIdx.x; i < D; i += kGenThreads) c.x[i] = c.x[i] - M[tri(i, j)] * xj;
+    for (int i = j + 1 + threadIdx.x; i < D; i += kGenThreads) c.x[i] = c.x[i] - M[rowp(i) + j] * xj;
     __syncthreads();
   }
   const double tol = 2.2250738585072014e-308;  // DBL_MIN
   for (int i = threadIdx.x; i < D; i += kGenThreads) {
-    const double d = M[tri(i, i)];
+    const double d = M[rowp(i) + i];
     c.x[i] = fabs(d) > tol ? c.x[i] / d : 0.0;
   }
   __syncthreads();
-  // backward substitution: s -= L_ji x_j for j ascending — a serial chain
-  if (threadIdx.x == 0) {
-    for (int i = D - 1; i >= 0; --i) {
-      double s = c.x[i];
-      for (int j = i + 1; j < D; ++j) s -= M[tri(j, i)] * c.x[j];
-      c.x[i] = s;
-    }
+  // backward substitution, column sweep (oracle.cpp ldlt_solve: x_i -= L_ji x_j
+  // for j = D-1 down to 1)
+  for (int j = D - 1; j > 0; --j) {
+    const double xj = c.x[j];
+    const double* Mj = M + rowp(j);
+    for (int i = threadIdx.x; i < j; i += kGenThreads) c.x[i] = c.x[i] - Mj[i] * xj;
+    __syncthreads();
   }
-  __syncthreads();
   for (int p = threadIdx.x; p < D; p += kGenThreads) c.dl[c.ord[p]] = c.x[p];  // P^T y
   __syncthreads();
 }
 
 // gauss_newton (local_opt.cpp:20-82) on one block. Returns false if the start
 // is infeasible / non-finite (the reference throws).
-__device__ bool block_gn(const DevState& S, const Blk& k, const Carve& c, double* M,
-                         unsigned long long cnt[3]) {
+// Model FLOPs per event (sincos, div, sqrt count 1), by block size:
+// GN trial: LDLT D^3/3 + solves and M fill ~2.5 D^2 + residuals/objective
+// ~260 per observation; GN Jacobian + g + H_ii ~400 per observation + 4 D;
+// L-BFGS value ~100/obs + 10 D, gradient ~350/obs + 4 D, direction 4 h D + 8 D,
+// accepted pair ~12 D.
+__device__ __forceinline__ unsigned long long fl_trial(const Blk& k) {
+  const unsigned long long D = (unsigned long long)k.D;
+  return D * D * D / 3 + 5 * D * D / 2 + 260ull * k.nobs;
+}
+
+template <bool kSharedM>
+__device__ __forceinline__ bool block_gn(const DevState& S, const Blk& k, const Carve& c, double* M,
+                                         unsigned long long cnt[6]) {
   const int D = k.D;
   if (threadIdx.x < 8) c.flag[threadIdx.x] = 0;
   __syncthreads();
@@ -433,7 +464,10 @@ __device__ bool block_gn(const DevState& S, const Blk& k, const Carve& c, double
     jacobians(S, k, c, c.v);
     __syncthreads();
     if (c.flag[1]) return true;  // kSingular: x unchanged
-    if (threadIdx.x == 0) ++cnt[0];
+    if (threadIdx.x == 0) {
+      ++cnt[0];
+      cnt[5] += 400ull * k.nobs + 4ull * D;
+    }
     // g = 2 J^T r, rows in order; H_ii
     for (int i = threadIdx.x; i < D; i += kGenThreads) {
       bool pt;
@@ -470,7 +504,7 @@ __device__ bool block_gn(const DevState& S, const Blk& k, const Carve& c, double
         c.hd[i] = lambda > 0.0 ? h + lambda * damp : h;
       }
       __syncthreads();
-      ldlt_solve(k, c, M);
+      ldlt_solve<kSharedM>(k, c, kSharedM ? c.M : M);
       if (threadIdx.x < 8) c.flag[threadIdx.x] = 0;
       __syncthreads();
       for (int i = threadIdx.x; i < D; i += kGenThreads) {
@@ -479,6 +513,7 @@ __device__ bool block_gn(const DevState& S, const Blk& k, const Carve& c, double
       }
       __syncthreads();
       bool accepted = false;
+      if (threadIdx.x == 0) cnt[5] += fl_trial(k);
       if (!c.flag[4]) {
         if (threadIdx.x == 0) ++cnt[1];
         residuals(S, k, c, c.vt, c.rt);
@@ -524,7 +559,7 @@ __device__ __forceinline__ double huber_value(double e0, double e1, double delta
 }
 
 // value at V into *out (thread 0); flag[0] set if infeasible. Residuals in rr.
-__device__ void h_value(const DevState& S, const Blk& k, const Carve& c, const double* V,
+__device__ __forceinline__ void h_value(const DevState& S, const Blk& k, const Carve& c, const double* V,
                         double* rr, double* out) {
   residuals(S, k, c, V, rr);
   __syncthreads();
@@ -550,7 +585,7 @@ __device__ void h_value(const DevState& S, const Blk& k, const Carve& c, const d
 }
 
 // gradient at V into G (flag[1] set if infeasible).
-__device__ void h_grad(const DevState& S, const Blk& k, const Carve& c, const double* V, double* G) {
+__device__ __forceinline__ void h_grad(const DevState& S, const Blk& k, const Carve& c, const double* V, double* G) {
   for (int o = threadIdx.x; o < k.nobs; o += kGenThreads) {
     exact::ETrig t;
     double R[9], w[3], z[2], v9[9];
@@ -601,8 +636,8 @@ __device__ void h_grad(const DevState& S, const Blk& k, const Carve& c, const do
   __syncthreads();
 }
 
-__device__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
-                            unsigned long long cnt[5]) {
+__device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
+                            unsigned long long cnt[6]) {
   const int D = k.D;
   const int mem = S.lbfgs_memory;
   if (threadIdx.x < 8) c.flag[threadIdx.x] = 0;
@@ -614,6 +649,7 @@ __device__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
     for (int i = 0; i < D; ++i) ok = ok && isfinite(c.g[i]);
     c.flag[2] = ok ? 0 : 1;
     ++cnt[0];
+    cnt[5] += 450ull * k.nobs + 14ull * D;
   }
   __syncthreads();
   if (c.flag[2]) return false;
@@ -642,6 +678,7 @@ __device__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
         }
         ++cnt[3];
         cnt[4] += h_size;
+        cnt[5] += (4ull * h_size + 8ull) * D;
         for (int i = 0; i < D; ++i) c.dl[i] = -c.x[i];
         double slope = seq_dot(c.g, c.dl, D);
         c.flag[4] = 0;
@@ -667,6 +704,7 @@ __device__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
       if (threadIdx.x == 0) {
         c.flag[0] = 0;
         ++cnt[1];
+        cnt[5] += 100ull * k.nobs + 10ull * D;
       }
       __syncthreads();
       h_value(S, k, c, c.vt, c.rt, &c.red[2]);
@@ -690,6 +728,7 @@ __device__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
       if (fin) {
         ++cnt[0];
         ++cnt[2];
+        cnt[5] += 350ull * k.nobs + 16ull * D;
         // s = trial - x (in c.x), y = g_new - g (in c.dl)
         for (int i = 0; i < D; ++i) {
           c.x[i] = c.vt[i] - c.v[i];
@@ -747,15 +786,18 @@ __device__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
 }
 
 // ---- K1G: persistent CTAs, one block at a time ----------------------------
-__global__ void __launch_bounds__(kGenThreads) k_local_blocks(DevState S, GenState G,
+#ifndef DBAG_GEN_MINB
+#define DBAG_GEN_MINB 4  // 128 registers: 4 CTAs per SM when shared memory allows
+#endif
+__global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(DevState S, GenState G,
                                                               int64_t begin, int64_t count) {
   extern __shared__ __align__(16) char smem_raw[];
   Carve c;
   carve(smem_raw, G.max_dim, G.max_np, G.max_nc, G.max_nobs,
         S.loss == DBAG_LOSS_HUBER ? S.lbfgs_memory : 0, G.m_in_smem != 0, &c);
-  double* M = G.m_in_smem ? c.M : G.mscratch + (size_t)blockIdx.x * tri(G.max_dim, 0);
+  double* M = G.m_in_smem ? nullptr : G.mscratch + (size_t)blockIdx.x * tri(G.max_dim, 0);
   __shared__ int64_t next;
-  unsigned long long cnt[5] = {0, 0, 0, 0, 0};
+  unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
   for (;;) {
     if (threadIdx.x == 0) next = (int64_t)atomicAdd(G.work, 1ull);
     __syncthreads();
@@ -831,7 +873,11 @@ __global__ void __launch_bounds__(kGenThreads) k_local_blocks(DevState S, GenSta
       for (int o = 0; o < k.nobs; ++o) c.pto[c.ord[c.opl[o]]++] = o;
     }
     __syncthreads();
-    const bool ok = huber ? block_lbfgs(S, k, c, cnt) : block_gn(S, k, c, M, cnt);
+    // M in shared memory: the instantiation that reads c.M directly, so every
+    // access compiles to LDS/STS (a shared-or-global pointer forces generic LD).
+    const bool ok = huber ? block_lbfgs(S, k, c, cnt)
+                          : (G.m_in_smem ? block_gn<true>(S, k, c, nullptr, cnt)
+                                         : block_gn<false>(S, k, c, M, cnt));
     __syncthreads();
     if (!ok) {
       if (threadIdx.x == 0)
@@ -851,7 +897,7 @@ __global__ void __launch_bounds__(kGenThreads) k_local_blocks(DevState S, GenSta
   }
   if (threadIdx.x == 0) {
     unsigned long long* slot = S.counters + 8 * (blockIdx.x % kCounterStripes);
-    for (int m = 0; m < 5; ++m)
+    for (int m = 0; m < 6; ++m)
       if (cnt[m]) atomicAdd(slot + m, cnt[m]);
   }
 }

@@ -1275,6 +1275,7 @@ int dbag_get_round_stats(dbag_solver* h, dbag_round_stats* out) {
       s.n_accept += c[8 * k + 2];
       s.n_direction += c[8 * k + 3];
       s.n_pairs_used += c[8 * k + 4];
+      s.n_model_flops += c[8 * k + 5];
     }
     // profiling on: sums over the profiled rounds since the last reset;
     // otherwise the last round.
