@@ -179,6 +179,11 @@ struct AdmmResult {
   Trace trace;
 };
 
+// LocalBlock (admm_solver.hpp:35-45).
+struct LocalBlock {
+  std::vector<int32_t> point_ids, cam_ids, obs_ids, obs_point_local, obs_cam_local;
+};
+
 class AdmmSolver {
  public:
   AdmmSolver(const Problem& problem, const ParamState& init, const AdmmOptions& opts,
@@ -262,6 +267,27 @@ class AdmmSolver {
   int64_t comm_floats_per_iteration() const { return dbag_comm_floats(h_); }
   int64_t num_blocks() const { return dbag_num_blocks(h_); }
   dbag_solver* handle() const { return h_; }
+
+  // blocks() (admm_solver.hpp:108)
+  std::vector<LocalBlock> blocks() const {
+    const int64_t B = num_blocks();
+    int64_t pc = 0, cc = 0;
+    check(dbag_num_copies(h_, &pc, &cc));
+    std::vector<int64_t> oo(B + 1), po(B + 1), co(B + 1);
+    std::vector<int32_t> pid(pc), cid(cc), obs(l_), opl(l_), ocl(l_);
+    check(dbag_get_blocks(h_, oo.data(), po.data(), pid.data(), co.data(), cid.data(), opl.data(),
+                          ocl.data()));
+    check(dbag_get_block_order(h_, obs.data()));
+    std::vector<LocalBlock> out(B);
+    for (int64_t b = 0; b < B; ++b) {
+      out[b].point_ids.assign(pid.begin() + po[b], pid.begin() + po[b + 1]);
+      out[b].cam_ids.assign(cid.begin() + co[b], cid.begin() + co[b + 1]);
+      out[b].obs_ids.assign(obs.begin() + oo[b], obs.begin() + oo[b + 1]);
+      out[b].obs_point_local.assign(opl.begin() + oo[b], opl.begin() + oo[b + 1]);
+      out[b].obs_cam_local.assign(ocl.begin() + oo[b], ocl.begin() + oo[b + 1]);
+    }
+    return out;
+  }
 
  private:
   std::pair<double, double> primal() const {

@@ -170,3 +170,28 @@ def test_general_blocks_reject_sharding(O, P):
     with pytest.raises(P.Unsupported):
         P.AdmmSolver.sharded(gprob, P.ParamState(ip, s.cam_f, ix),
                              P.AdmmOptions(points_per_block=2), 0, 2)
+
+
+def test_cpp_driver_with_block_config(O, P):
+    """tools/dbag_solve over include/dbag.hpp with BlockConfig{8,2} on config 1:
+    the metrics CSV equals the oracle's trajectory with the same BlockConfig."""
+    import os
+    import subprocess
+    from paper_1708_07954_b200 import build as b
+    exe = b.TOOL_BIN if os.path.exists(b.TOOL_BIN) else b.build_tools()
+    out = subprocess.run([exe, "1", "6", "l2", "exact", "1.0", "8", "2"], capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    rows = [r.split(",") for r in out.stdout.strip().splitlines()[1:]]
+    s = P.generate_config_scene(1, 0, 1.0)
+    p = s.problem
+    oprob = O.Problem.create(p.cam_pose, p.cam_f, p.points, p.obs_cam, p.obs_pt, p.obs_uv)
+    osol = O.AdmmSolver(oprob, s.init.cam_pose, p.cam_f, s.init.points, points_per_block=8,
+                        cameras_per_block=2, max_iters=6)
+    ot = osol.run(s.ground_truth.cam_pose, s.ground_truth.points)
+    assert len(rows) == len(ot) == 6
+    for f, o in zip(rows, ot):
+        assert int(f[0]) == o["iter"] and int(f[7]) == o["comm_floats"]
+        assert float(f[2]) == o["max_primal_x"] and float(f[3]) == o["max_primal_y"]
+        a = float(f[1])
+        assert a == o["mean_reproj_err"] or abs(a - o["mean_reproj_err"]) <= 1e-12 * abs(a)

@@ -1,7 +1,9 @@
 // dbag_solve — C++ host driver over the drop-in header (include/dbag.hpp):
 // what `dba solve --solver admm` (tools/dba_main.cpp:231-259) does, on the B200.
-//   dbag_solve <config 1..5> <rounds> [l2|huber] [exact|fast] [scale]
-//       generate a BASELINE config scene, solve, print the metrics CSV
+//   dbag_solve <config 1..5> <rounds> [l2|huber] [exact|fast] [scale] [points_per_block]
+//              [cameras_per_block]
+//       generate a BASELINE config scene, solve (BlockConfig, default {1,1}),
+//       print the metrics CSV
 //   dbag_solve file <problem.txt> <rounds> [l2|huber] [exact|fast] [solved.txt] [metrics.csv]
 //       parse a reference problem file (bal_io.hpp format), solve from its
 //       record, write the solved problem and the metrics CSV (metrics_csv.hpp)
@@ -91,6 +93,9 @@ int main(int argc, char** argv) {
   const bool huber = argc > 3 && std::strcmp(argv[3], "huber") == 0;
   const bool fast = argc > 4 && std::strcmp(argv[4], "fast") == 0;
   const double scale = argc > 5 ? std::atof(argv[5]) : 1.0;
+  dba::gpu::BlockConfig blocks;
+  blocks.points_per_block = argc > 6 ? std::atoi(argv[6]) : 1;
+  blocks.cameras_per_block = argc > 7 ? std::atoi(argv[7]) : 1;
   dbag_scene* sc = nullptr;
   dbag_scene_info info{};
   if (dbag_scene_generate(config, 0, scale, &sc, &info) != DBAG_OK) {
@@ -120,7 +125,7 @@ int main(int argc, char** argv) {
   opts.numerics = fast ? DBAG_NUMERICS_FAST : DBAG_NUMERICS_EXACT;
   try {
     const dba::gpu::ParamState truth = problem.nominal_state();
-    const dba::gpu::AdmmResult res = dba::gpu::run_admm(problem, init, opts, {}, &truth);
+    const dba::gpu::AdmmResult res = dba::gpu::run_admm(problem, init, opts, blocks, &truth);
     std::printf("iter,mean_reproj_err,max_primal_x,max_primal_y,camera_mse,point_mse,wall_ms,comm_floats\n");
     for (const auto& r : res.trace)
       std::printf("%d,%.17g,%.17g,%.17g,%.17g,%.17g,%.6g,%lld\n", r.iter, r.mean_reproj_err,
