@@ -15,6 +15,8 @@ VARIANTS = {
     "exact_minb2": ["-DDBAG_K1E_MINB=2"],
     "exact_minb3": ["-DDBAG_K1E_MINB=3"],
     "exact_minb4": ["-DDBAG_K1E_MINB=4"],
+    "jcache0": ["-DDBAG_K1E_JCACHE=0"],
+    "jcache1": ["-DDBAG_K1E_JCACHE=1"],
 }
 
 
