@@ -202,6 +202,14 @@ int64_t dbag_comm_floats(dbag_solver* h);        /* comm_floats_per_iteration() 
 /* problem.hpp:59-85 at the current consensus. */
 int dbag_mean_reprojection_error(dbag_solver* h, double* out); /* throws-variant semantics */
 int dbag_total_squared_error(dbag_solver* h, double* out);
+int dbag_rms_reprojection_error(dbag_solver* h, double* out); /* problem.cpp:159-162 */
+/* align_similarity (problem.cpp:204-237): Umeyama similarity of state's points
+ * onto reference's, applied to points and cameras (f kept). Host views in,
+ * host arrays out ([m][6], [n][3]); moments reduced on `device`. Tolerance
+ * parity (Eigen's JacobiSVD is not bit-pinnable). SizeMismatch if the point
+ * counts differ or n < 3. */
+int dbag_align_similarity(const dbag_param_view* state, const dbag_param_view* reference,
+                          int32_t device, double* out_pose, double* out_points);
 
 /* Measurement hooks (no reference analogue): enqueue one full round
  * (local+consensus+dual+metrics) on the handle's stream without waiting;

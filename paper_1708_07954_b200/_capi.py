@@ -104,6 +104,9 @@ SIGNATURES = {
     "dbag_num_blocks": (C.c_int64, [H]),
     "dbag_get_block_order": (C.c_int, [H, I32P]),
     "dbag_num_copies": (C.c_int, [H, I64P, I64P]),
+    "dbag_rms_reprojection_error": (C.c_int, [H, DPTR]),
+    "dbag_align_similarity": (C.c_int, [C.POINTER(ParamView), C.POINTER(ParamView), C.c_int32,
+                                        DPTR, DPTR]),
     "dbag_get_blocks": (C.c_int, [H, I64P, I64P, I32P, I64P, I32P, I32P, I32P]),
     "dbag_partition": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int32, C.POINTER(H),
                                  I64P, I64P, I64P, I64P]),

@@ -271,6 +271,19 @@ def _partition_arrays(problem, points_per_block, cameras_per_block):
     return (obs_off, obs_ids, pt_off, pt_ids, cam_off, cam_ids, opl, ocl), comm.value
 
 
+def align_similarity(state: ParamState, reference: ParamState, device: int = 0) -> ParamState:
+    """align_similarity (problem.hpp:87-90, problem.cpp:204-237): the similarity
+    gauge that maps state's points onto reference's (Umeyama), applied to
+    points and cameras; focal lengths are kept."""
+    st, ref = state.copy(), reference.copy()
+    m, n = len(st.cam_f), len(st.points)
+    pose, pts = np.zeros((m, 6)), np.zeros((n, 3))
+    sv, rv = st._view(), ref._view()
+    _check(_capi.load().dbag_align_similarity(C.byref(sv), C.byref(rv), device, _dp(pose),
+                                              _dp(pts)))
+    return ParamState(pose, st.cam_f.copy(), pts)
+
+
 def partition(problem, points_per_block=1, cameras_per_block=1):
     """partition() (admm_solver.hpp:47, admm_solver.cpp:14-72): list of LocalBlock."""
     arrays, _ = _partition_arrays(problem, points_per_block, cameras_per_block)
@@ -472,6 +485,11 @@ class AdmmSolver:
     def mean_reprojection_error(self):
         out = C.c_double()
         _check(self._lib.dbag_mean_reprojection_error(self._h, C.byref(out)))
+        return out.value
+
+    def rms_reprojection_error(self):
+        out = C.c_double()
+        _check(self._lib.dbag_rms_reprojection_error(self._h, C.byref(out)))
         return out.value
 
     def total_squared_error(self):

@@ -21,10 +21,11 @@ for _p in sys.path + [os.path.join(sys.prefix, "lib", "python3.12", "site-packag
         break
 NCCL_INC = ["-I", os.path.join(NCCL_HOME, "include")] if NCCL_HOME else []
 SOURCES = [("dbag_capi.cu", NCCL_INC), ("dbag_exact.cu", ["-fmad=false"]),
-           ("dbag_blocks.cu", ["-fmad=false"]),
+           ("dbag_blocks.cu", ["-fmad=false"]), ("dbag_metrics.cu", ["-fmad=false"]),
            ("dbag_scenes.cpp", []), ("dbag_shard.cpp", []), ("dbag_io.cpp", [])]
 HEADERS = ["dbag_common.cuh", "dbag_local.cuh", "dbag_lbfgs.cuh", "dbag_consensus.cuh",
-           "dbag_index.cuh", "dbag_exact.h", "dbag_shard.h", "dbag_exact_geom.cuh", "dbag_blocks.h"]
+           "dbag_index.cuh", "dbag_exact.h", "dbag_shard.h", "dbag_exact_geom.cuh", "dbag_blocks.h",
+           "dbag_metrics.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -17,6 +17,7 @@
 #include "dbag_common.cuh"
 #include "dbag_consensus.cuh"
 #include "dbag_blocks.h"
+#include "dbag_metrics.h"
 #include "dbag_exact.h"
 #include "dbag_shard.h"
 #include <nccl.h>
@@ -1212,6 +1213,23 @@ int dbag_mean_reprojection_error(dbag_solver* h, double* out) {
   return guarded([&] {
     CK(cudaSetDevice(h->device));
     *out = h->reproj_sum(1, true) / (double)h->S.L;
+  });
+}
+
+int dbag_rms_reprojection_error(dbag_solver* h, double* out) {  // problem.cpp:159-162
+  return guarded([&] {
+    CK(cudaSetDevice(h->device));
+    *out = std::sqrt(h->reproj_sum(2, true) / (double)h->S.L);
+  });
+}
+
+int dbag_align_similarity(const dbag_param_view* state, const dbag_param_view* reference,
+                          int32_t device, double* out_pose, double* out_points) {
+  return guarded([&] {
+    std::string msg;
+    const int rc =
+        metrics::align_similarity(state, reference, device, out_pose, out_points, &msg);
+    if (rc != DBAG_OK) raise(rc, msg);
   });
 }
 
