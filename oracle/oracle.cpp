@@ -1145,6 +1145,244 @@ std::vector<IterationRecord> AdmmSolver::run(const ParamState* ref) {
 }
 
 // ---------------------------------------------------------------------------
+// centralized LM — proj/src/lm_solver.cpp
+// ---------------------------------------------------------------------------
+namespace {
+// lm_solver.cpp:17-25: undamped normal-equation blocks, row-major storage.
+struct NormalEquations {
+  std::vector<std::array<double, 36>> U;  // per camera, 6x6
+  std::vector<std::array<double, 9>> V;   // per point, 3x3
+  std::vector<std::array<double, 18>> W;  // per observation, 6x3 = A^T B
+  VecX g_cam, g_pt;
+  std::vector<std::vector<std::pair<int, int>>> point_obs;  // per point: (cam, obs)
+};
+
+// lm_solver.cpp:27-57. A = J_camera (2x6), B = J_point (2x3), r = z - pi.
+// Products A^T A etc. as 2-term sums over the rows (r = 0 then 1).
+bool assemble(const Problem& p, const ParamState& s, const Guard& g, NormalEquations* eq) {
+  const int m = p.num_cameras(), n = p.num_points();
+  eq->U.assign(m, {});
+  eq->V.assign(n, {});
+  eq->W.assign(p.num_observations(), {});
+  eq->g_cam.assign(6 * (size_t)m, 0.0);
+  eq->g_pt.assign(3 * (size_t)n, 0.0);
+  eq->point_obs.assign(n, {});
+  for (int k = 0; k < p.num_observations(); ++k) {
+    const Observation& ob = p.observations[k];
+    Expansion e;
+    if (!try_project_with_jacobians(s.points[ob.point_id], s.cameras[ob.cam_id], g, &e))
+      return false;
+    const double r[2] = {ob.z[0] - e.z[0], ob.z[1] - e.z[1]};
+    auto& U = eq->U[ob.cam_id];
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j) U[6 * i + j] += e.Jc[0][i] * e.Jc[0][j] + e.Jc[1][i] * e.Jc[1][j];
+    auto& V = eq->V[ob.point_id];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) V[3 * i + j] += e.Jp[0][i] * e.Jp[0][j] + e.Jp[1][i] * e.Jp[1][j];
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 3; ++j)
+        eq->W[k][3 * i + j] = e.Jc[0][i] * e.Jp[0][j] + e.Jc[1][i] * e.Jp[1][j];
+    for (int i = 0; i < 6; ++i)
+      eq->g_cam[6 * (size_t)ob.cam_id + i] += e.Jc[0][i] * r[0] + e.Jc[1][i] * r[1];
+    for (int i = 0; i < 3; ++i)
+      eq->g_pt[3 * (size_t)ob.point_id + i] += e.Jp[0][i] * r[0] + e.Jp[1][i] * r[1];
+    eq->point_obs[ob.point_id].push_back({ob.cam_id, k});
+  }
+  return true;
+}
+
+// lm_solver.cpp:59-127
+LmStep solve_step(const NormalEquations& eq, int m, int n, double lambda, bool use_schur) {
+  std::vector<std::array<double, 36>> U = eq.U;
+  for (int j = 0; j < m; ++j)
+    for (int d = 0; d < 6; ++d) U[j][7 * d] += lambda * eq.U[j][7 * d];
+  std::vector<std::array<double, 9>> V = eq.V;
+  for (int i = 0; i < n; ++i)
+    for (int d = 0; d < 3; ++d) V[i][4 * d] += lambda * eq.V[i][4 * d];
+  LmStep step;
+  if (use_schur) {
+    std::vector<std::array<double, 9>> Vinv(n);
+    for (int i = 0; i < n; ++i) {  // V.ldlt().solve(I)
+      MatX Vm(3, 3);
+      for (int k = 0; k < 9; ++k) Vm.a[k] = V[i][k];
+      for (int c = 0; c < 3; ++c) {
+        VecX e(3, 0.0);
+        e[c] = 1.0;
+        const VecX col = ldlt_solve(Vm, e);
+        for (int r = 0; r < 3; ++r) Vinv[i][3 * r + c] = col[r];
+      }
+    }
+    const int D = 6 * m;
+    MatX S(D, D);
+    for (int j = 0; j < m; ++j)
+      for (int r = 0; r < 6; ++r)
+        for (int c = 0; c < 6; ++c) S(6 * j + r, 6 * j + c) = U[j][6 * r + c];
+    VecX rhs = eq.g_cam;
+    for (int i = 0; i < n; ++i) {
+      const auto& owners = eq.point_obs[i];
+      double vg[3];
+      for (int r = 0; r < 3; ++r)
+        vg[r] = (Vinv[i][3 * r] * eq.g_pt[3 * (size_t)i] + Vinv[i][3 * r + 1] * eq.g_pt[3 * (size_t)i + 1]) +
+                Vinv[i][3 * r + 2] * eq.g_pt[3 * (size_t)i + 2];
+      for (const auto& [ja, ka] : owners) {
+        const auto& Wa = eq.W[ka];
+        for (int r = 0; r < 6; ++r)
+          rhs[6 * (size_t)ja + r] -= (Wa[3 * r] * vg[0] + Wa[3 * r + 1] * vg[1]) + Wa[3 * r + 2] * vg[2];
+        double WV[18];
+        for (int r = 0; r < 6; ++r)
+          for (int c = 0; c < 3; ++c)
+            WV[3 * r + c] = (Wa[3 * r] * Vinv[i][c] + Wa[3 * r + 1] * Vinv[i][3 + c]) +
+                            Wa[3 * r + 2] * Vinv[i][6 + c];
+        for (const auto& [jb, kb] : owners) {
+          const auto& Wb = eq.W[kb];
+          for (int r = 0; r < 6; ++r)
+            for (int c = 0; c < 6; ++c)
+              S(6 * ja + r, 6 * jb + c) -=
+                  (WV[3 * r] * Wb[3 * c] + WV[3 * r + 1] * Wb[3 * c + 1]) + WV[3 * r + 2] * Wb[3 * c + 2];
+        }
+      }
+    }
+    step.delta_cameras = ldlt_solve(S, rhs);
+    step.delta_points.assign(3 * (size_t)n, 0.0);
+    for (int i = 0; i < n; ++i) {
+      double acc[3] = {eq.g_pt[3 * (size_t)i], eq.g_pt[3 * (size_t)i + 1], eq.g_pt[3 * (size_t)i + 2]};
+      for (const auto& [j, k] : eq.point_obs[i]) {
+        const auto& Wk = eq.W[k];
+        const double* dc = &step.delta_cameras[6 * (size_t)j];
+        for (int c = 0; c < 3; ++c) {  // W^T dc: 6-term sums in order
+          double s = 0.0;
+          for (int r = 0; r < 6; ++r) s += Wk[3 * r + c] * dc[r];
+          acc[c] -= s;
+        }
+      }
+      for (int r = 0; r < 3; ++r)
+        step.delta_points[3 * (size_t)i + r] =
+            (Vinv[i][3 * r] * acc[0] + Vinv[i][3 * r + 1] * acc[1]) + Vinv[i][3 * r + 2] * acc[2];
+    }
+  } else {
+    const int dim = 6 * m + 3 * n;
+    MatX H(dim, dim);
+    for (int j = 0; j < m; ++j)
+      for (int r = 0; r < 6; ++r)
+        for (int c = 0; c < 6; ++c) H(6 * j + r, 6 * j + c) = U[j][6 * r + c];
+    for (int i = 0; i < n; ++i)
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) H(6 * m + 3 * i + r, 6 * m + 3 * i + c) = V[i][3 * r + c];
+    for (int i = 0; i < n; ++i)
+      for (const auto& [j, k] : eq.point_obs[i])
+        for (int r = 0; r < 6; ++r)
+          for (int c = 0; c < 3; ++c) {
+            H(6 * j + r, 6 * m + 3 * i + c) = eq.W[k][3 * r + c];
+            H(6 * m + 3 * i + c, 6 * j + r) = eq.W[k][3 * r + c];
+          }
+    VecX g(dim);
+    for (int k = 0; k < 6 * m; ++k) g[k] = eq.g_cam[k];
+    for (int k = 0; k < 3 * n; ++k) g[6 * (size_t)m + k] = eq.g_pt[k];
+    const VecX delta = ldlt_solve(H, g);
+    step.delta_cameras.assign(delta.begin(), delta.begin() + 6 * (size_t)m);
+    step.delta_points.assign(delta.begin() + 6 * (size_t)m, delta.end());
+  }
+  return step;
+}
+
+// lm_solver.cpp:129-138
+ParamState apply_step(const ParamState& s, const LmStep& st) {
+  ParamState out = s;
+  for (size_t j = 0; j < out.cameras.size(); ++j) {
+    Vec6 p = out.cameras[j].pose();
+    for (int k = 0; k < 6; ++k) p[k] += st.delta_cameras[6 * j + k];
+    out.cameras[j].set_pose(p);
+  }
+  for (size_t i = 0; i < out.points.size(); ++i)
+    for (int k = 0; k < 3; ++k) out.points[i][k] += st.delta_points[3 * i + k];
+  return out;
+}
+
+double total_squared_error_throwing(const Problem& p, const ParamState& s, const Guard& g) {
+  double t = 0.0;
+  if (try_total_squared_error(p, s, g, &t)) return t;
+  mean_reprojection_error(p, s, g);  // throws with the offending indices
+  return 0.0;
+}
+}  // namespace
+
+// lm_solver.cpp:142-151
+LmStep lm_compute_step(const Problem& p, const ParamState& s, double lambda, bool use_schur,
+                       const Guard& g) {
+  NormalEquations eq;
+  if (!assemble(p, s, g, &eq)) {
+    mean_reprojection_error(p, s, g);
+    throw DepthBelowGuard(0.0, g.eps_depth);
+  }
+  return solve_step(eq, p.num_cameras(), p.num_points(), lambda, use_schur);
+}
+
+// lm_solver.cpp:153-218
+LmResult solve_lm(const Problem& p, const ParamState& init, const LmOptions& o, const Loss& loss,
+                  const ParamState* ref) {
+  if (loss.is_huber()) throw ValidationError("the LM baseline supports only the squared L2 loss");
+  const int m = p.num_cameras(), n = p.num_points();
+  LmResult out;
+  out.state = init;
+  double total = total_squared_error_throwing(p, out.state, o.guard);
+  auto record = [&](int iter, double wall_ms) {
+    IterationRecord rec;
+    rec.iter = iter;
+    rec.mean_reproj_err = mean_reprojection_error(p, out.state, o.guard);
+    if (ref != nullptr) {
+      const MseResult mse = parameter_mse(out.state, *ref);
+      rec.camera_mse = mse.camera_mse;
+      rec.point_mse = mse.point_mse;
+    }
+    rec.wall_ms = wall_ms;
+    out.trace.push_back(rec);
+  };
+  record(0, 0.0);
+  double lambda = o.lambda_init;
+  for (int iter = 1; iter <= o.max_iters; ++iter) {
+    if (total < o.error_stop) {
+      out.stop = kLmErrorStop;
+      return out;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    NormalEquations eq;
+    if (!assemble(p, out.state, o.guard, &eq)) {
+      mean_reprojection_error(p, out.state, o.guard);
+      throw DepthBelowGuard(0.0, o.guard.eps_depth);
+    }
+    bool accepted = false;
+    while (!accepted) {
+      const LmStep step = solve_step(eq, m, n, lambda, o.use_schur);
+      bool fin = true;
+      for (double v : step.delta_cameras) fin = fin && std::isfinite(v);
+      for (double v : step.delta_points) fin = fin && std::isfinite(v);
+      if (fin) {
+        const ParamState trial = apply_step(out.state, step);
+        double tt = 0.0;
+        if (try_total_squared_error(p, trial, o.guard, &tt) && tt < total) {
+          out.state = trial;
+          total = tt;
+          lambda = std::max(lambda / o.lambda_down, 1e-12);
+          ++out.accepted_steps;
+          accepted = true;
+          break;
+        }
+      }
+      lambda *= o.lambda_up;
+      if (lambda > o.lambda_max) {
+        out.stop = kLmLambdaMax;
+        return out;
+      }
+    }
+    const double wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    record(iter, wall_ms);
+  }
+  out.stop = total < o.error_stop ? kLmErrorStop : kLmMaxIters;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
 // rng + scene generation — proj/include/dba/rng.hpp, proj/src/scene_gen.cpp
 // ---------------------------------------------------------------------------
 // proj/include/dba/rng.hpp:26-30

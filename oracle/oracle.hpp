@@ -268,6 +268,33 @@ class AdmmSolver {
   std::unique_ptr<WorkerPool> pool_;
 };
 
+// ---- centralized LM baseline (proj/include/dba/lm_solver.hpp, proj/src/lm_solver.cpp)
+struct LmOptions {
+  int max_iters = 100;
+  double error_stop = 1e-14;
+  double lambda_init = 1e-3;
+  double lambda_max = 1e16;
+  double lambda_up = 10.0;
+  double lambda_down = 10.0;
+  bool use_schur = true;
+  Guard guard;
+};
+enum LmStopReason { kLmErrorStop = 0, kLmLambdaMax = 1, kLmMaxIters = 2 };
+struct LmStep {
+  VecX delta_cameras;  // 6m
+  VecX delta_points;   // 3n
+};
+struct LmResult {
+  ParamState state;
+  std::vector<IterationRecord> trace;
+  int stop = kLmMaxIters;
+  int accepted_steps = 0;
+};
+LmStep lm_compute_step(const Problem& p, const ParamState& s, double lambda, bool use_schur,
+                       const Guard& g);
+LmResult solve_lm(const Problem& p, const ParamState& init, const LmOptions& o, const Loss& loss,
+                  const ParamState* reference);
+
 // ---- rng + scene generation (proj/include/dba/rng.hpp, proj/src/scene_gen.cpp)
 class Rng {
  public:

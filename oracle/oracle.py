@@ -330,6 +330,46 @@ def rng_draw(seed, kind, count, arg=0):
     return out
 
 
+# ---- centralized LM (lm_solver.cpp) ---------------------------------------------
+class LmOptions(C.Structure):
+    _fields_ = [("max_iters", C.c_int), ("error_stop", C.c_double), ("lambda_init", C.c_double),
+                ("lambda_max", C.c_double), ("lambda_up", C.c_double),
+                ("lambda_down", C.c_double), ("use_schur", C.c_int), ("eps_depth", C.c_double)]
+
+
+def lm_options(**kw):
+    o = LmOptions()
+    lib().orc_lm_options_default(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def solve_lm(problem, pose, f, pts, options=None, loss=0, ref_pose=None, ref_pts=None, **kw):
+    """solve_lm (lm_solver.hpp:51-54): returns (pose, pts, trace, stop, accepted)."""
+    o = options if options is not None else lm_options(**kw)
+    m, n = len(f), len(pts)
+    out_pose, out_pts = np.zeros((m, 6)), np.zeros((n, 3))
+    cap = o.max_iters + 2
+    tr = (Record * cap)()
+    nt, stop, acc = C.c_int(), C.c_int(), C.c_int()
+    check(lib().orc_lm_solve(problem.h, _p(_f64(pose)), _p(_f64(f)), _p(_f64(pts)), C.byref(o),
+                             loss, _p(None if ref_pose is None else _f64(ref_pose)),
+                             _p(None if ref_pts is None else _f64(ref_pts)), _p(out_pose),
+                             _p(out_pts), tr, cap, C.byref(nt), C.byref(stop), C.byref(acc)))
+    return out_pose, out_pts, [tr[k].as_dict() for k in range(min(nt.value, cap))], stop.value, \
+        acc.value
+
+
+def lm_compute_step(problem, pose, f, pts, lam, use_schur=True, eps=1e-6):
+    m, n = len(f), len(pts)
+    dc, dp = np.zeros(6 * m), np.zeros(3 * n)
+    check(lib().orc_lm_compute_step(problem.h, _p(_f64(pose)), _p(_f64(f)), _p(_f64(pts)),
+                                    C.c_double(lam), int(use_schur), C.c_double(eps), _p(dc),
+                                    _p(dp)))
+    return dc, dp
+
+
 # ---- ADMM solver -------------------------------------------------------------
 class AdmmSolver:
     """Reference ``AdmmSolver`` (proj/include/dba/admm_solver.hpp:75-138)."""

@@ -593,6 +593,73 @@ double orc_admm_block_objective(void* h, int b) { return S(h).block_objective(b)
 long long orc_admm_ops_per_iteration(void* h) { return S(h).ops_per_iteration(); }
 long long orc_admm_comm_floats(void* h) { return S(h).comm_floats_per_iteration(); }
 
+// ---- centralized LM (lm_solver.cpp)
+typedef struct {
+  int max_iters;
+  double error_stop, lambda_init, lambda_max, lambda_up, lambda_down;
+  int use_schur;
+  double eps_depth;
+} orc_lm_options;
+
+void orc_lm_options_default(orc_lm_options* o) {
+  const LmOptions d;
+  o->max_iters = d.max_iters;
+  o->error_stop = d.error_stop;
+  o->lambda_init = d.lambda_init;
+  o->lambda_max = d.lambda_max;
+  o->lambda_up = d.lambda_up;
+  o->lambda_down = d.lambda_down;
+  o->use_schur = d.use_schur ? 1 : 0;
+  o->eps_depth = d.guard.eps_depth;
+}
+
+static LmOptions lm_opts_from(const orc_lm_options* o) {
+  LmOptions r;
+  r.max_iters = o->max_iters;
+  r.error_stop = o->error_stop;
+  r.lambda_init = o->lambda_init;
+  r.lambda_max = o->lambda_max;
+  r.lambda_up = o->lambda_up;
+  r.lambda_down = o->lambda_down;
+  r.use_schur = o->use_schur != 0;
+  r.guard.eps_depth = o->eps_depth;
+  return r;
+}
+
+int orc_lm_solve(void* hp, const double* pose, const double* f, const double* pts,
+                 const orc_lm_options* o, int loss_type, const double* ref_pose,
+                 const double* ref_pts, double* out_pose, double* out_pts, orc_record* trace,
+                 int cap, int* n_trace, int* stop, int* accepted) {
+  return guarded([&] {
+    const Problem& p = *static_cast<Problem*>(hp);
+    const int m = p.num_cameras(), n = p.num_points();
+    const ParamState init = state_from(m, n, pose, f, pts);
+    ParamState ref;
+    if (ref_pose) ref = state_from(m, n, ref_pose, f, ref_pts);
+    Loss loss;
+    loss.type = loss_type;
+    const LmResult r = solve_lm(p, init, lm_opts_from(o), loss, ref_pose ? &ref : nullptr);
+    state_to(r.state, out_pose, nullptr, out_pts);
+    *n_trace = (int)r.trace.size();
+    for (int k = 0; k < (int)r.trace.size() && k < cap; ++k) rec_to(r.trace[k], trace + k);
+    *stop = r.stop;
+    *accepted = r.accepted_steps;
+  });
+}
+
+int orc_lm_compute_step(void* hp, const double* pose, const double* f, const double* pts,
+                        double lambda, int use_schur, double eps_depth, double* dc, double* dp) {
+  return guarded([&] {
+    const Problem& p = *static_cast<Problem*>(hp);
+    Guard g;
+    g.eps_depth = eps_depth;
+    const LmStep st = lm_compute_step(p, state_from(p.num_cameras(), p.num_points(), pose, f, pts),
+                                      lambda, use_schur != 0, g);
+    std::memcpy(dc, st.delta_cameras.data(), sizeof(double) * st.delta_cameras.size());
+    std::memcpy(dp, st.delta_points.data(), sizeof(double) * st.delta_points.size());
+  });
+}
+
 int orc_partition_count(void* hp, int ppb, int cpb, int* nblocks) {
   return guarded([&] { *nblocks = (int)partition(*static_cast<Problem*>(hp), {ppb, cpb}).size(); });
 }
