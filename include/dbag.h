@@ -282,6 +282,34 @@ int dbag_exchange_copy(dbag_solver* dst, dbag_solver* src, int32_t which);
  * distortion; 3 per point) followed by Problem::create validation. serialize:
  * 17 significant digits (bit-exact round trip), observations from `problem`,
  * cameras/points from `state`. Two-phase outputs: buf NULL -> *len only. */
+/* ---- centralized Levenberg-Marquardt baseline (lm_solver.hpp:13-54,
+ * lm_solver.cpp): Schur complement on the device, the dense 6m x 6m camera
+ * system by cuSOLVER. Tolerance parity (Eigen's blocked LDLT is not
+ * bit-pinnable). DESIGN.md §12. */
+typedef struct {
+  int32_t max_iters;     /* LmOptions (lm_solver.hpp:14-23) */
+  double error_stop, lambda_init, lambda_max, lambda_up, lambda_down;
+  int32_t use_schur;     /* 0: the dense (6m+3n) step, <= 24000 unknowns */
+  double eps_depth;      /* ProjectionGuard */
+  int32_t device;
+} dbag_lm_options;
+typedef enum { DBAG_LM_ERROR_STOP = 0, DBAG_LM_LAMBDA_MAX = 1, DBAG_LM_MAX_ITERS = 2 } dbag_lm_stop;
+typedef struct dbag_lm dbag_lm;
+void dbag_lm_options_default(dbag_lm_options* o);
+/* Problem::create validation + the initial state (copied to the device). */
+int dbag_lm_create(const dbag_problem_view* problem, const dbag_param_view* init,
+                   const dbag_lm_options* opts, dbag_lm** out);
+/* solve_lm (lm_solver.cpp:153-218) from the handle's state; trace[0] is the
+ * init row; loss must be DBAG_LOSS_SQUARED_L2; reference nullable (MSE). */
+int dbag_lm_solve(dbag_lm* h, int32_t loss, const dbag_param_view* reference,
+                  dbag_iteration_record* trace, int64_t cap, int64_t* n_trace, int32_t* stop,
+                  int32_t* accepted_steps);
+/* lm_compute_step (lm_solver.cpp:142-151) at the handle's state. */
+int dbag_lm_compute_step(dbag_lm* h, double lambda, int32_t use_schur, double* d_cam /*[6m]*/,
+                         double* d_pts /*[3n]*/);
+int dbag_lm_get_state(dbag_lm* h, double* cam_pose /*[m][6]*/, double* points /*[n][3]*/);
+void dbag_lm_destroy(dbag_lm* h);
+
 /* ---- host-only: partition() and communication_cost() (admm_solver.hpp:47-54,
  * admm_solver.cpp:14-101) for any BlockConfig. No GPU needed. */
 typedef struct dbag_partition_result dbag_partition_result;

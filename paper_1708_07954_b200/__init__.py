@@ -6,9 +6,11 @@ from .admm import (AdmmOptions, AdmmSolver, AdmmState, DepthBelowGuard, DeviceEr
                    ParamState, Problem, Scene, SingularSystem, SizeMismatch, Unsupported,
                    ValidationError, generate_config_scene, run_admm, ParseError,
                    parse_problem_text, serialize_problem_text, metrics_csv,
-                   LocalBlock, partition, communication_cost, align_similarity)
+                   LocalBlock, partition, communication_cost, align_similarity,
+                   LmOptions, LmResult, solve_lm, lm_compute_step)
 from ._capi import load as load_library  # noqa: F401
 
 __all__ = ["AdmmOptions", "AdmmSolver", "AdmmState", "ParamState", "Problem", "LossKind",
            "InnerOptions", "run_admm", "generate_config_scene", "load_library", "LocalBlock",
-           "partition", "communication_cost", "align_similarity"]
+           "partition", "communication_cost", "align_similarity", "LmOptions", "LmResult", "solve_lm",
+           "lm_compute_step"]

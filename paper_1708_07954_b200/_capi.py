@@ -66,6 +66,13 @@ class SceneInfo(C.Structure):
                 ("sigma_init", C.c_double)]
 
 
+class LmOptions(C.Structure):
+    _fields_ = [("max_iters", C.c_int32), ("error_stop", C.c_double), ("lambda_init", C.c_double),
+                ("lambda_max", C.c_double), ("lambda_up", C.c_double),
+                ("lambda_down", C.c_double), ("use_schur", C.c_int32), ("eps_depth", C.c_double),
+                ("device", C.c_int32)]
+
+
 class ShardInfo(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("cam_begin", C.c_int32),
                 ("cam_end", C.c_int32), ("local_obs", C.c_int64), ("local_points", C.c_int32),
@@ -104,6 +111,14 @@ SIGNATURES = {
     "dbag_num_blocks": (C.c_int64, [H]),
     "dbag_get_block_order": (C.c_int, [H, I32P]),
     "dbag_num_copies": (C.c_int, [H, I64P, I64P]),
+    "dbag_lm_options_default": (None, [C.POINTER(LmOptions)]),
+    "dbag_lm_create": (C.c_int, [C.POINTER(ProblemView), C.POINTER(ParamView),
+                                 C.POINTER(LmOptions), C.POINTER(H)]),
+    "dbag_lm_solve": (C.c_int, [H, C.c_int32, C.POINTER(ParamView), C.POINTER(IterationRecord),
+                                C.c_int64, I64P, I32P, I32P]),
+    "dbag_lm_compute_step": (C.c_int, [H, C.c_double, C.c_int32, DPTR, DPTR]),
+    "dbag_lm_get_state": (C.c_int, [H, DPTR, DPTR]),
+    "dbag_lm_destroy": (None, [H]),
     "dbag_rms_reprojection_error": (C.c_int, [H, DPTR]),
     "dbag_align_similarity": (C.c_int, [C.POINTER(ParamView), C.POINTER(ParamView), C.c_int32,
                                         DPTR, DPTR]),

@@ -284,6 +284,80 @@ def align_similarity(state: ParamState, reference: ParamState, device: int = 0) 
     return ParamState(pose, st.cam_f.copy(), pts)
 
 
+@dataclass
+class LmOptions:
+    """LmOptions (lm_solver.hpp:14-23) + device."""
+    max_iters: int = 100
+    error_stop: float = 1e-14
+    lambda_init: float = 1e-3
+    lambda_max: float = 1e16
+    lambda_up: float = 10.0
+    lambda_down: float = 10.0
+    use_schur: bool = True
+    eps_depth: float = 1e-6
+    device: int = 0
+
+    def _c(self):
+        o = _capi.LmOptions()
+        _capi.load().dbag_lm_options_default(C.byref(o))
+        for k in ("max_iters", "error_stop", "lambda_init", "lambda_max", "lambda_up",
+                  "lambda_down", "eps_depth", "device"):
+            setattr(o, k, getattr(self, k))
+        o.use_schur = int(self.use_schur)
+        return o
+
+
+@dataclass
+class LmResult:
+    """LmResult (lm_solver.hpp:33-38)."""
+    state: ParamState
+    trace: list
+    stop: int  # 0 error stop, 1 lambda max, 2 max iters (LmStopReason)
+    accepted_steps: int
+
+
+class _LmHandle:
+    def __init__(self, problem, state, opts):
+        self._lib = _capi.load()
+        self._h = C.c_void_p()
+        st = state.copy()
+        pv, iv, o = problem._view(), st._view(), opts._c()
+        _check(self._lib.dbag_lm_create(C.byref(pv), C.byref(iv), C.byref(o), C.byref(self._h)))
+        self.m, self.n, self.f = problem.num_cameras, problem.num_points, st.cam_f.copy()
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.dbag_lm_destroy(self._h)
+
+
+def solve_lm(problem, init, opts=None, loss=None, reference=None) -> LmResult:
+    """solve_lm (lm_solver.hpp:51-54) on the device."""
+    opts = opts or LmOptions()
+    loss = loss or LossKind()
+    h = _LmHandle(problem, init, opts)
+    cap = opts.max_iters + 2
+    tr = (_capi.IterationRecord * cap)()
+    nt, stop, acc = C.c_int64(), C.c_int32(), C.c_int32()
+    rv = None
+    if reference is not None:
+        ref = reference.copy()
+        rv = C.byref(ref._view())
+    _check(h._lib.dbag_lm_solve(h._h, loss.type, rv, tr, cap, C.byref(nt), C.byref(stop),
+                                C.byref(acc)))
+    pose, pts = np.zeros((h.m, 6)), np.zeros((h.n, 3))
+    _check(h._lib.dbag_lm_get_state(h._h, _dp(pose), _dp(pts)))
+    return LmResult(ParamState(pose, h.f, pts), [tr[k].as_dict() for k in range(min(nt.value, cap))],
+                    stop.value, acc.value)
+
+
+def lm_compute_step(problem, state, lam, use_schur=True, eps_depth=1e-6, device=0):
+    """lm_compute_step (lm_solver.hpp:47-48): (delta_cameras [6m], delta_points [3n])."""
+    h = _LmHandle(problem, state, LmOptions(eps_depth=eps_depth, device=device))
+    dc, dp = np.zeros(6 * h.m), np.zeros(3 * h.n)
+    _check(h._lib.dbag_lm_compute_step(h._h, lam, int(use_schur), _dp(dc), _dp(dp)))
+    return dc, dp
+
+
 def partition(problem, points_per_block=1, cameras_per_block=1):
     """partition() (admm_solver.hpp:47, admm_solver.cpp:14-72): list of LocalBlock."""
     arrays, _ = _partition_arrays(problem, points_per_block, cameras_per_block)

@@ -22,10 +22,11 @@ for _p in sys.path + [os.path.join(sys.prefix, "lib", "python3.12", "site-packag
 NCCL_INC = ["-I", os.path.join(NCCL_HOME, "include")] if NCCL_HOME else []
 SOURCES = [("dbag_capi.cu", NCCL_INC), ("dbag_exact.cu", ["-fmad=false"]),
            ("dbag_blocks.cu", ["-fmad=false"]), ("dbag_metrics.cu", ["-fmad=false"]),
+           ("dbag_lm.cu", ["-fmad=false"]),
            ("dbag_scenes.cpp", []), ("dbag_shard.cpp", []), ("dbag_io.cpp", [])]
 HEADERS = ["dbag_common.cuh", "dbag_local.cuh", "dbag_lbfgs.cuh", "dbag_consensus.cuh",
            "dbag_index.cuh", "dbag_exact.h", "dbag_shard.h", "dbag_exact_geom.cuh", "dbag_blocks.h",
-           "dbag_metrics.h"]
+           "dbag_metrics.h", "dbag_errors.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -71,8 +72,10 @@ def build(force=False, verbose=False, extra=()):
     if not NCCL_HOME:
         raise RuntimeError("NCCL headers/library (nvidia/nccl in site-packages) not found")
     ncclib = os.path.join(NCCL_HOME, "lib")
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(nvcc())), "lib64")
     cmd = [nvcc(), *ARCH, "-shared", *objs, "-o", LIB + ".tmp", "-L", ncclib, "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + ncclib]
+           "-Xlinker", "-rpath," + ncclib, "-L", cudalib, "-lcusolver", "-lcublas",
+           "-Xlinker", "-rpath," + cudalib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -77,6 +77,23 @@ int guarded(F&& f) {
 
 [[noreturn]] void raise(int code, const std::string& msg) { throw StatusError{code, msg}; }
 
+}  // namespace
+
+// Error reporting for the other C-ABI translation units (dbag_lm.cu):
+// dbag_last_error / dbag_last_error_info read what this sets.
+namespace dbag {
+int set_error(int code, const std::string& msg, int32_t point_id, int32_t cam_id, double depth) {
+  g_err = code == DBAG_OK ? std::string() : msg;
+  g_err_pt = point_id;
+  g_err_cam = cam_id;
+  g_err_depth = depth;
+  g_err_block = -1;
+  return code;
+}
+}  // namespace dbag
+
+namespace {
+
 inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 template <typename T>

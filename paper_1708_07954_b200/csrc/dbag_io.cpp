@@ -180,6 +180,26 @@ void validate_problem(int m, int n, const std::vector<int32_t>& cam, const std::
       fail(DBAG_ERR_VALIDATION, "point " + std::to_string(i) + " is observed by no camera");
 }
 
+}  // namespace
+
+namespace dbag {
+int validate_problem_arrays(int m, int n, int64_t l, const int32_t* cam, const int32_t* pt,
+                            const double* uv, const double* pose, const double* f,
+                            const double* pts, std::string* msg) {
+  try {
+    validate_problem(m, n, std::vector<int32_t>(cam, cam + l), std::vector<int32_t>(pt, pt + l),
+                     std::vector<double>(uv, uv + 2 * l), std::vector<double>(pose, pose + 6 * (size_t)m),
+                     std::vector<double>(f, f + m), std::vector<double>(pts, pts + 3 * (size_t)n));
+  } catch (const IoError& e) {
+    *msg = e.msg;
+    return e.code;
+  }
+  return DBAG_OK;
+}
+}  // namespace dbag
+
+namespace {
+
 template <typename F>
 int guarded(F&& f) {
   try {
