@@ -370,11 +370,20 @@ def our_arm(args, rank, world, local_rank):
     kernels["local"]["frac_fp64"] = kernels["local"]["tflops"] / fp64_peak
     kernels["local"]["flops_per_obs"] = fl / Lr
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    traffic = None  # ncu dram bytes per K1 launch, committed for the default workload
+    if (dom == "local" and not general and args.numerics == "exact" and args.loss == "l2"
+            and args.config == 5 and world == 1):
+        try:
+            t = json.load(open(os.path.join(ROOT, "profiles", "r1_k1_traffic_config5.json")))
+            traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+        except (OSError, ValueError, KeyError):
+            traffic = None
     if dom == "local":
         roof = {"kernel": ("k_local_blocks (K1, generalized blocks, model FLOPs counted per block)"
                            if general else "k_local (K1 local solve)"), "bound": "fp64",
                 "achieved": kernels["local"]["tflops"], "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": kernels["local"]["frac_fp64"], "traffic": None,
+                "frac": kernels["local"]["frac_fp64"], "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (ncu, profiles/r1_k1_traffic_config5.json)",
                 "peak_source": "measured on this device by dbag_measure_fp64_peak (DFMA probe); "
                                "MEASURED_PEAKS.json has no FP64 figure",
                 "hbm_frac_same_kernel": kernels["local"]["frac_hbm"]}
