@@ -98,6 +98,10 @@ int64_t communication_cost(const Partition& P, int32_t M, int32_t N) {
 // device: shared-memory carve-out of one CTA
 // ---------------------------------------------------------------------------
 constexpr int kGenThreads = 128;
+#ifndef DBAG_WARP_BLOCK_MAX_DIM
+#define DBAG_WARP_BLOCK_MAX_DIM 64
+#endif
+constexpr int kWarpBlockMaxDim = DBAG_WARP_BLOCK_MAX_DIM;  // D at or below: a warp per block
 constexpr double kDampingInit = 1e-4;  // local_opt.cpp:13
 constexpr double kDampingMax = 1e12;   // local_opt.cpp:14
 
@@ -161,6 +165,21 @@ __host__ __device__ inline size_t carve(char* base, int D, int NP, int NC, int N
 }
 
 // ---------------------------------------------------------------------------
+// Thread groups: kT = 128 (a CTA per block) or 32 (a warp per block, for small
+// blocks: four blocks per CTA, warp barriers).
+template <int kT>
+__device__ __forceinline__ int gtid() {
+  return kT == kGenThreads ? (int)threadIdx.x : (int)(threadIdx.x & (kT - 1));
+}
+template <int kT>
+__device__ __forceinline__ void gsync() {
+  if (kT == 32)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
 // device: one block's problem
 // ---------------------------------------------------------------------------
 struct Blk {
@@ -200,9 +219,10 @@ __device__ __forceinline__ int jcol(bool pt, int co) { return pt ? co : 3 + co; 
 
 // Residuals at V for every observation (one thread each) into rr[2*nobs];
 // flag[0] := 1 if any projection is infeasible or any row is non-finite.
+template <int kT>
 __device__ __forceinline__ void residuals(const DevState& S, const Blk& k, const Carve& c, const double* V,
                           double* rr) {
-  for (int o = threadIdx.x; o < k.nobs; o += kGenThreads) {
+  for (int o = gtid<kT>(); o < k.nobs; o += kT) {
     exact::ETrig t;
     double R[9], w[3], z[2], v9[9];
     if (!gproject(S, k, c, V, o, t, R, w, z, v9)) {
@@ -217,8 +237,9 @@ __device__ __forceinline__ void residuals(const DevState& S, const Blk& k, const
 }
 
 // Jacobian rows (positive e.Jp | e.Jc, geometry.cpp:141-159) at V.
+template <int kT>
 __device__ __forceinline__ void jacobians(const DevState& S, const Blk& k, const Carve& c, const double* V) {
-  for (int o = threadIdx.x; o < k.nobs; o += kGenThreads) {
+  for (int o = gtid<kT>(); o < k.nobs; o += kT) {
     exact::ETrig t;
     double R[9], w[3], z[2], v9[9];
     if (!gproject(S, k, c, V, o, t, R, w, z, v9)) {
@@ -311,9 +332,10 @@ __device__ __forceinline__ double seq_dot(const double* a, const double* b, int 
 // position holding the largest value among k..D-1 (strict '>' from a[k]),
 // then a transposition. One warp; ord[p] = variable at position p. Scratch:
 // c.x (filled with the permuted right-hand side only afterwards).
+template <int kT>
 __device__ __forceinline__ void pivot_order(const Blk& k, const Carve& c) {
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
+  if (gtid<kT>() >= 32) return;
+  const int lane = gtid<kT>();
   double* a = c.x;
   for (int i = lane; i < k.D; i += 32) {
     a[i] = fabs(c.hd[i]);
@@ -359,13 +381,13 @@ __device__ __forceinline__ void pivot_order(const Blk& k, const Carve& c) {
 // Result in c.dl. Scratch: c.dl / c.vt (temp[] double buffer), c.hdg is kept.
 __device__ __forceinline__ int rowp(int i) { return i * (i + 1) / 2; }
 
-template <bool kSharedM>
+template <int kT, bool kSharedM>
 __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double* M) {
   const int D = k.D;
-  pivot_order(k, c);
-  __syncthreads();
+  pivot_order<kT>(k, c);
+  gsync<kT>();
   const int ne = rowp(D);
-  for (int e = threadIdx.x; e < ne; e += kGenThreads) {
+  for (int e = gtid<kT>(); e < ne; e += kT) {
     int p = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
     while (rowp(p + 1) <= e) ++p;
     while (rowp(p) > e) --p;
@@ -373,8 +395,8 @@ __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double*
     const int i = c.ord[p], j = c.ord[q];
     M[e] = p == q ? c.hd[i] : h_entry(k, c, i, j);
   }
-  for (int p = threadIdx.x; p < D; p += kGenThreads) c.x[p] = c.g[c.ord[p]];  // P rhs (g holds rhs)
-  __syncthreads();
+  for (int p = gtid<kT>(); p < D; p += kT) c.x[p] = c.g[c.ord[p]];  // P rhs (g holds rhs)
+  gsync<kT>();
   // Left-looking LDL^T, unpivoted (the permutation is already applied).
   // temp[j] = D_j L_kj for the next column is formed during this column's
   // division phase (double buffer), so each column costs two barriers.
@@ -384,53 +406,53 @@ __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double*
     const double* tc = tbuf[kk & 1];
     double* tn = tbuf[(kk + 1) & 1];
     if (kk > 0) {
-      for (int i = kk + threadIdx.x; i < D; i += kGenThreads) {
+      for (int i = kk + gtid<kT>(); i < D; i += kT) {
         double* Mi = M + rowp(i);
         double s = 0.0;
         for (int j = 0; j < kk; ++j) s += Mi[j] * tc[j];
         Mi[kk] = Mi[kk] - s;
       }
-      __syncthreads();
+      gsync<kT>();
     }
     const double akk = M[rowp(kk) + kk];
     const bool valid = fabs(akk) > 0.0;
     if (kk == 0 && !valid) {
       stop = true;  // Eigen: all-zero diagonal, nothing factorized
     } else {
-      for (int i = kk + 1 + threadIdx.x; i < D; i += kGenThreads) {
+      for (int i = kk + 1 + gtid<kT>(); i < D; i += kT) {
         double* Mi = M + rowp(i);
         if (valid) Mi[kk] = Mi[kk] / akk;
         if (i == kk + 1) tn[kk] = M[rowp(kk) + kk] * Mi[kk];  // D_kk L_{kk+1,kk}
       }
       if (kk + 1 < D) {
         const double* Mn = M + rowp(kk + 1);
-        for (int j = threadIdx.x; j < kk; j += kGenThreads) tn[j] = M[rowp(j) + j] * Mn[j];
+        for (int j = gtid<kT>(); j < kk; j += kT) tn[j] = M[rowp(j) + j] * Mn[j];
       }
     }
-    __syncthreads();
+    gsync<kT>();
   }
   // forward substitution, column sweep (same per-row order as the oracle)
   for (int j = 0; j < D - 1; ++j) {
     const double xj = c.x[j];
-    for (int i = j + 1 + threadIdx.x; i < D; i += kGenThreads) c.x[i] = c.x[i] - M[rowp(i) + j] * xj;
-    __syncthreads();
+    for (int i = j + 1 + gtid<kT>(); i < D; i += kT) c.x[i] = c.x[i] - M[rowp(i) + j] * xj;
+    gsync<kT>();
   }
   const double tol = 2.2250738585072014e-308;  // DBL_MIN
-  for (int i = threadIdx.x; i < D; i += kGenThreads) {
+  for (int i = gtid<kT>(); i < D; i += kT) {
     const double d = M[rowp(i) + i];
     c.x[i] = fabs(d) > tol ? c.x[i] / d : 0.0;
   }
-  __syncthreads();
+  gsync<kT>();
   // backward substitution, column sweep (oracle.cpp ldlt_solve: x_i -= L_ji x_j
   // for j = D-1 down to 1)
   for (int j = D - 1; j > 0; --j) {
     const double xj = c.x[j];
     const double* Mj = M + rowp(j);
-    for (int i = threadIdx.x; i < j; i += kGenThreads) c.x[i] = c.x[i] - Mj[i] * xj;
-    __syncthreads();
+    for (int i = gtid<kT>(); i < j; i += kT) c.x[i] = c.x[i] - Mj[i] * xj;
+    gsync<kT>();
   }
-  for (int p = threadIdx.x; p < D; p += kGenThreads) c.dl[c.ord[p]] = c.x[p];  // P^T y
-  __syncthreads();
+  for (int p = gtid<kT>(); p < D; p += kT) c.dl[c.ord[p]] = c.x[p];  // P^T y
+  gsync<kT>();
 }
 
 // gauss_newton (local_opt.cpp:20-82) on one block. Returns false if the start
@@ -445,31 +467,31 @@ __device__ __forceinline__ unsigned long long fl_trial(const Blk& k) {
   return D * D * D / 3 + 5 * D * D / 2 + 260ull * k.nobs;
 }
 
-template <bool kSharedM>
+template <int kT, bool kSharedM>
 __device__ __forceinline__ bool block_gn(const DevState& S, const Blk& k, const Carve& c, double* M,
                                          unsigned long long cnt[6]) {
   const int D = k.D;
-  if (threadIdx.x < 8) c.flag[threadIdx.x] = 0;
-  __syncthreads();
-  residuals(S, k, c, c.v, c.r);
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (gtid<kT>() < 8) c.flag[gtid<kT>()] = 0;
+  gsync<kT>();
+  residuals<kT>(S, k, c, c.v, c.r);
+  gsync<kT>();
+  if (gtid<kT>() == 0) {
     const bool ok = c.flag[0] == 0 && weight_rows_finite(k, c, c.v);
     c.flag[2] = ok ? 0 : 1;
     if (ok) c.red[0] = objective_rows(k, c, c.r, c.v);
   }
-  __syncthreads();
+  gsync<kT>();
   if (c.flag[2]) return false;
   for (int it = 0; it < S.inner_max_iters; ++it) {
-    jacobians(S, k, c, c.v);
-    __syncthreads();
+    jacobians<kT>(S, k, c, c.v);
+    gsync<kT>();
     if (c.flag[1]) return true;  // kSingular: x unchanged
-    if (threadIdx.x == 0) {
+    if (gtid<kT>() == 0) {
       ++cnt[0];
       cnt[5] += 400ull * k.nobs + 4ull * D;
     }
     // g = 2 J^T r, rows in order; H_ii
-    for (int i = threadIdx.x; i < D; i += kGenThreads) {
+    for (int i = gtid<kT>(); i < D; i += kT) {
       bool pt;
       int idx, co;
       var_of(k, i, pt, idx, co);
@@ -490,35 +512,35 @@ __device__ __forceinline__ bool block_gn(const DevState& S, const Blk& k, const 
       c.g[i] = 2.0 * s;
       c.hdg[i] = h;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) c.flag[3] = sqrt(seq_dot(c.g, c.g, D)) <= S.grad_tol;
-    __syncthreads();
+    gsync<kT>();
+    if (gtid<kT>() == 0) c.flag[3] = sqrt(seq_dot(c.g, c.g, D)) <= S.grad_tol;
+    gsync<kT>();
     if (c.flag[3]) return true;  // kGradConverged
-    for (int i = threadIdx.x; i < D; i += kGenThreads) c.g[i] = -0.5 * c.g[i];  // rhs
+    for (int i = gtid<kT>(); i < D; i += kT) c.g[i] = -0.5 * c.g[i];  // rhs
     double lambda = 0.0;
     bool next = false;
     while (!next) {
-      for (int i = threadIdx.x; i < D; i += kGenThreads) {
+      for (int i = gtid<kT>(); i < D; i += kT) {
         const double h = c.hdg[i];
         const double damp = h < 1e-12 ? 1e-12 : h;  // std::max(H_ii, 1e-12)
         c.hd[i] = lambda > 0.0 ? h + lambda * damp : h;
       }
-      __syncthreads();
-      ldlt_solve<kSharedM>(k, c, kSharedM ? c.M : M);
-      if (threadIdx.x < 8) c.flag[threadIdx.x] = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < D; i += kGenThreads) {
+      gsync<kT>();
+      ldlt_solve<kT, kSharedM>(k, c, kSharedM ? c.M : M);
+      if (gtid<kT>() < 8) c.flag[gtid<kT>()] = 0;
+      gsync<kT>();
+      for (int i = gtid<kT>(); i < D; i += kT) {
         if (!isfinite(c.dl[i])) c.flag[4] = 1;
         c.vt[i] = c.v[i] + c.dl[i];
       }
-      __syncthreads();
+      gsync<kT>();
       bool accepted = false;
-      if (threadIdx.x == 0) cnt[5] += fl_trial(k);
+      if (gtid<kT>() == 0) cnt[5] += fl_trial(k);
       if (!c.flag[4]) {
-        if (threadIdx.x == 0) ++cnt[1];
-        residuals(S, k, c, c.vt, c.rt);
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        if (gtid<kT>() == 0) ++cnt[1];
+        residuals<kT>(S, k, c, c.vt, c.rt);
+        gsync<kT>();
+        if (gtid<kT>() == 0) {
           c.flag[5] = 0;
           if (c.flag[0] == 0 && weight_rows_finite(k, c, c.vt)) {
             const double objt = objective_rows(k, c, c.rt, c.vt);
@@ -528,18 +550,18 @@ __device__ __forceinline__ bool block_gn(const DevState& S, const Blk& k, const 
             }
           }
         }
-        __syncthreads();
+        gsync<kT>();
         accepted = c.flag[5] != 0;
       }
       if (accepted) {
-        for (int i = threadIdx.x; i < D; i += kGenThreads) c.v[i] = c.vt[i];
-        for (int n = threadIdx.x; n < 2 * k.nobs; n += kGenThreads) c.r[n] = c.rt[n];
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        for (int i = gtid<kT>(); i < D; i += kT) c.v[i] = c.vt[i];
+        for (int n = gtid<kT>(); n < 2 * k.nobs; n += kT) c.r[n] = c.rt[n];
+        gsync<kT>();
+        if (gtid<kT>() == 0) {
           ++cnt[2];
           c.flag[6] = sqrt(seq_dot(c.dl, c.dl, D)) <= S.step_tol * (1.0 + sqrt(seq_dot(c.v, c.v, D)));
         }
-        __syncthreads();
+        gsync<kT>();
         if (c.flag[6]) return true;  // kStepConverged
         next = true;
       } else {
@@ -559,11 +581,12 @@ __device__ __forceinline__ double huber_value(double e0, double e1, double delta
 }
 
 // value at V into *out (thread 0); flag[0] set if infeasible. Residuals in rr.
+template <int kT>
 __device__ __forceinline__ void h_value(const DevState& S, const Blk& k, const Carve& c, const double* V,
                         double* rr, double* out) {
-  residuals(S, k, c, V, rr);
-  __syncthreads();
-  if (threadIdx.x == 0 && c.flag[0] == 0) {
+  residuals<kT>(S, k, c, V, rr);
+  gsync<kT>();
+  if (gtid<kT>() == 0 && c.flag[0] == 0) {
     double total = 0.0;
     for (int o = 0; o < k.nobs; ++o) total += huber_value(rr[2 * o], rr[2 * o + 1], S.huber_delta);
     for (int q = 0; q < k.np; ++q) {
@@ -581,12 +604,13 @@ __device__ __forceinline__ void h_value(const DevState& S, const Blk& k, const C
     }
     *out = total;
   }
-  __syncthreads();
+  gsync<kT>();
 }
 
 // gradient at V into G (flag[1] set if infeasible).
+template <int kT>
 __device__ __forceinline__ void h_grad(const DevState& S, const Blk& k, const Carve& c, const double* V, double* G) {
-  for (int o = threadIdx.x; o < k.nobs; o += kGenThreads) {
+  for (int o = gtid<kT>(); o < k.nobs; o += kT) {
     exact::ETrig t;
     double R[9], w[3], z[2], v9[9];
     if (!gproject(S, k, c, V, o, t, R, w, z, v9)) {
@@ -617,8 +641,8 @@ __device__ __forceinline__ void h_grad(const DevState& S, const Blk& k, const Ca
     c.lg[2 * o] = l0;
     c.lg[2 * o + 1] = l1;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < k.D; i += kGenThreads) {
+  gsync<kT>();
+  for (int i = gtid<kT>(); i < k.D; i += kT) {
     bool pt;
     int idx, co;
     var_of(k, i, pt, idx, co);
@@ -633,31 +657,32 @@ __device__ __forceinline__ void h_grad(const DevState& S, const Blk& k, const Ca
     g += c.hd[i] + (pt ? S.rho_x : S.rho_y) * (V[i] - c.piv[i]);
     G[i] = g;
   }
-  __syncthreads();
+  gsync<kT>();
 }
 
+template <int kT>
 __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, const Carve& c,
                             unsigned long long cnt[6]) {
   const int D = k.D;
   const int mem = S.lbfgs_memory;
-  if (threadIdx.x < 8) c.flag[threadIdx.x] = 0;
-  __syncthreads();
-  h_value(S, k, c, c.v, c.r, &c.red[0]);
-  h_grad(S, k, c, c.v, c.g);
-  if (threadIdx.x == 0) {
+  if (gtid<kT>() < 8) c.flag[gtid<kT>()] = 0;
+  gsync<kT>();
+  h_value<kT>(S, k, c, c.v, c.r, &c.red[0]);
+  h_grad<kT>(S, k, c, c.v, c.g);
+  if (gtid<kT>() == 0) {
     bool ok = c.flag[0] == 0 && c.flag[1] == 0 && isfinite(c.red[0]);
     for (int i = 0; i < D; ++i) ok = ok && isfinite(c.g[i]);
     c.flag[2] = ok ? 0 : 1;
     ++cnt[0];
     cnt[5] += 450ull * k.nobs + 14ull * D;
   }
-  __syncthreads();
+  gsync<kT>();
   if (c.flag[2]) return false;
   int h_first = 0, h_size = 0;  // ring buffer, oldest at h_first (uniform)
   double gamma = 1.0;
   for (int it = 0; it < S.inner_max_iters; ++it) {
     // q in c.x, direction d in c.dl; the two-loop recursion on thread 0
-    if (threadIdx.x == 0) {
+    if (gtid<kT>() == 0) {
       c.flag[3] = sqrt(seq_dot(c.g, c.g, D)) <= S.grad_tol;
       if (!c.flag[3]) {
         for (int i = 0; i < D; ++i) c.x[i] = c.g[i];
@@ -690,7 +715,7 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
         c.red[1] = slope;
       }
     }
-    __syncthreads();
+    gsync<kT>();
     if (c.flag[3]) return true;  // kGradConverged
     if (c.flag[4]) {
       h_size = 0;
@@ -700,17 +725,17 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
     double step = 1.0;
     bool accepted = false;
     for (int ls = 0; ls < S.max_line_search; ++ls) {
-      for (int i = threadIdx.x; i < D; i += kGenThreads) c.vt[i] = c.v[i] + step * c.dl[i];
-      if (threadIdx.x == 0) {
+      for (int i = gtid<kT>(); i < D; i += kT) c.vt[i] = c.v[i] + step * c.dl[i];
+      if (gtid<kT>() == 0) {
         c.flag[0] = 0;
         ++cnt[1];
         cnt[5] += 100ull * k.nobs + 10ull * D;
       }
-      __syncthreads();
-      h_value(S, k, c, c.vt, c.rt, &c.red[2]);
+      gsync<kT>();
+      h_value<kT>(S, k, c, c.vt, c.rt, &c.red[2]);
       const bool ok = c.flag[0] == 0 && isfinite(c.red[2]) &&
                       c.red[2] <= c.red[0] + S.armijo_c * step * c.red[1];
-      __syncthreads();
+      gsync<kT>();
       if (ok) {
         accepted = true;
         break;
@@ -718,10 +743,10 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
       step *= S.backtrack;
     }
     if (!accepted) return true;  // kLineSearchFailed, best iterate kept
-    if (threadIdx.x == 0) c.flag[1] = 0;
-    __syncthreads();
-    h_grad(S, k, c, c.vt, c.hdg);  // g_new in hdg
-    if (threadIdx.x == 0) {
+    if (gtid<kT>() == 0) c.flag[1] = 0;
+    gsync<kT>();
+    h_grad<kT>(S, k, c, c.vt, c.hdg);  // g_new in hdg
+    if (gtid<kT>() == 0) {
       bool fin = c.flag[1] == 0;
       for (int i = 0; i < D; ++i) fin = fin && isfinite(c.hdg[i]);
       c.flag[5] = fin;
@@ -769,7 +794,7 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
         c.flag[7] = sn <= S.step_tol * (1.0 + sqrt(seq_dot(c.v, c.v, D)));
       }
     }
-    __syncthreads();
+    gsync<kT>();
     if (!c.flag[5]) return true;  // kLineSearchFailed
     gamma = c.red[3];
     if (c.flag[6]) {
@@ -780,7 +805,7 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
       }
     }
     if (c.flag[7]) return true;  // kStepConverged
-    __syncthreads();
+    gsync<kT>();
   }
   return true;  // kMaxIters
 }
@@ -789,20 +814,26 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
 #ifndef DBAG_GEN_MINB
 #define DBAG_GEN_MINB 4  // 128 registers: 4 CTAs per SM when shared memory allows
 #endif
-__global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(DevState S, GenState G,
-                                                              int64_t begin, int64_t count) {
+// kT threads per block: 128 (one block per CTA) or 32 (four per CTA, one per
+// warp, each with its own shared slice of group_bytes).
+template <int kT>
+__global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(
+    DevState S, GenState G, int64_t begin, int64_t count, size_t group_bytes) {
+  constexpr int kGroups = kGenThreads / kT;
   extern __shared__ __align__(16) char smem_raw[];
+  const int grp = (int)threadIdx.x / kT;
   Carve c;
-  carve(smem_raw, G.max_dim, G.max_np, G.max_nc, G.max_nobs,
+  carve(smem_raw + (size_t)grp * group_bytes, G.max_dim, G.max_np, G.max_nc, G.max_nobs,
         S.loss == DBAG_LOSS_HUBER ? S.lbfgs_memory : 0, G.m_in_smem != 0, &c);
-  double* M = G.m_in_smem ? nullptr : G.mscratch + (size_t)blockIdx.x * tri(G.max_dim, 0);
-  __shared__ int64_t next;
+  double* M = G.m_in_smem ? nullptr
+                          : G.mscratch + ((size_t)blockIdx.x * kGroups + grp) * tri(G.max_dim, 0);
+  __shared__ int64_t next[kGroups];
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
   for (;;) {
-    if (threadIdx.x == 0) next = (int64_t)atomicAdd(G.work, 1ull);
-    __syncthreads();
-    const int64_t idx = next;
-    __syncthreads();
+    if (gtid<kT>() == 0) next[grp] = (int64_t)atomicAdd(G.work, 1ull);
+    gsync<kT>();
+    const int64_t idx = next[grp];
+    gsync<kT>();
     if (idx >= count) break;
     Blk k;
     k.b = begin + idx;
@@ -819,7 +850,7 @@ __global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(Dev
     const bool huber = S.loss == DBAG_LOSS_HUBER;
     // load: copies, targets (x̄ - r/ρ: admm_solver.cpp:155-162) or, for Huber,
     // consensus (piv) and duals (hd); focal lengths; observations
-    for (int i = threadIdx.x; i < k.D; i += kGenThreads) {
+    for (int i = gtid<kT>(); i < k.D; i += kT) {
       double xb, du, rho;
       if (i < k.cb) {
         const int q = i / 3, m = i - 3 * q;
@@ -844,9 +875,9 @@ __global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(Dev
         c.tgt[i] = xb - du / rho;
       }
     }
-    for (int q = threadIdx.x; q < k.nc; q += kGenThreads)
+    for (int q = gtid<kT>(); q < k.nc; q += kT)
       c.fcam[q] = S.ybar[8 * (int64_t)G.cam_ids[k.c0 + q] + 6];
-    for (int o = threadIdx.x; o < k.nobs; o += kGenThreads) {
+    for (int o = gtid<kT>(); o < k.nobs; o += kT) {
       const int64_t s = k.o0 + o;
       const PointRec& rec = S.prec[S.blk_pos[s]];
       c.uv[2 * o] = rec.u;
@@ -854,8 +885,8 @@ __global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(Dev
       c.opl[o] = G.obs_pl[s];
       c.ocl[o] = G.obs_cl[s];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // observation lists per local point / camera
+    gsync<kT>();
+    if (gtid<kT>() == 0) {  // observation lists per local point / camera
       for (int q = 0; q <= k.np; ++q) c.pto_off[q] = 0;
       for (int q = 0; q <= k.nc; ++q) c.cmo_off[q] = 0;
       for (int o = 0; o < k.nobs; ++o) {
@@ -867,23 +898,23 @@ __global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(Dev
       for (int e = 0; e < k.np * k.nc; ++e) c.pco[e] = -1;
       for (int o = 0; o < k.nobs; ++o) c.pco[c.opl[o] * k.nc + c.ocl[o]] = o;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // counting-sort fill of the point lists (ascending o)
+    gsync<kT>();
+    if (gtid<kT>() == 0) {  // counting-sort fill of the point lists (ascending o)
       for (int q = 0; q < k.np; ++q) c.ord[q] = c.pto_off[q];
       for (int o = 0; o < k.nobs; ++o) c.pto[c.ord[c.opl[o]]++] = o;
     }
-    __syncthreads();
+    gsync<kT>();
     // M in shared memory: the instantiation that reads c.M directly, so every
     // access compiles to LDS/STS (a shared-or-global pointer forces generic LD).
-    const bool ok = huber ? block_lbfgs(S, k, c, cnt)
-                          : (G.m_in_smem ? block_gn<true>(S, k, c, nullptr, cnt)
-                                         : block_gn<false>(S, k, c, M, cnt));
-    __syncthreads();
+    const bool ok = huber ? block_lbfgs<kT>(S, k, c, cnt)
+                          : (G.m_in_smem ? block_gn<kT, true>(S, k, c, nullptr, cnt)
+                                         : block_gn<kT, false>(S, k, c, M, cnt));
+    gsync<kT>();
     if (!ok) {
-      if (threadIdx.x == 0)
+      if (gtid<kT>() == 0)
         atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)k.b);
     } else {  // write back (admm_solver.cpp:284-289)
-      for (int i = threadIdx.x; i < k.D; i += kGenThreads) {
+      for (int i = gtid<kT>(); i < k.D; i += kT) {
         if (i < k.cb) {
           const int q = i / 3, m = i - 3 * q;
           G.gx[(int64_t)m * G.PC + k.p0 + q] = c.v[i];
@@ -893,10 +924,10 @@ __global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(Dev
         }
       }
     }
-    __syncthreads();
+    gsync<kT>();
   }
-  if (threadIdx.x == 0) {
-    unsigned long long* slot = S.counters + 8 * (blockIdx.x % kCounterStripes);
+  if (gtid<kT>() == 0) {
+    unsigned long long* slot = S.counters + 8 * ((blockIdx.x * kGroups + grp) % kCounterStripes);
     for (int m = 0; m < 6; ++m)
       if (cnt[m]) atomicAdd(slot + m, cnt[m]);
   }
@@ -1245,17 +1276,28 @@ cudaError_t GenSolver::init(const DevState& S, int32_t ppb, int32_t cpb, int dev
   const size_t without_m =
       carve(nullptr, G.max_dim, G.max_np, G.max_nc, G.max_nobs, mem, false, nullptr);
   G.m_in_smem = (mem == 0 && with_m <= (size_t)max_optin) ? 1 : 0;
-  smem_bytes = G.m_in_smem ? with_m : without_m;
+  group_bytes = G.m_in_smem ? with_m : without_m;
+  // small blocks: a warp per block (its parallel phases are no wider than ~D)
+  warp_groups = G.max_dim <= kWarpBlockMaxDim && 4 * group_bytes <= (size_t)max_optin;
+  const int groups = warp_groups ? kGenThreads / 32 : 1;
+  smem_bytes = group_bytes * groups;
   if (smem_bytes > (size_t)max_optin) return cudaErrorInvalidConfiguration;
-  GK(cudaFuncSetAttribute(k_local_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem_bytes));
   int per_sm = 0, sms = 0;
-  GK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_blocks, kGenThreads,
-                                                   smem_bytes));
+  if (warp_groups) {
+    GK(cudaFuncSetAttribute(k_local_blocks<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem_bytes));
+    GK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_blocks<32>, kGenThreads,
+                                                     smem_bytes));
+  } else {
+    GK(cudaFuncSetAttribute(k_local_blocks<kGenThreads>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    GK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_blocks<kGenThreads>,
+                                                     kGenThreads, smem_bytes));
+  }
   GK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   resident = std::max(1, per_sm) * sms;
   if (!G.m_in_smem && mem == 0)
-    GK(dalloc(pool, &G.mscratch, (size_t)resident * (size_t)tri(G.max_dim, 0)));
+    GK(dalloc(pool, &G.mscratch, (size_t)resident * groups * (size_t)tri(G.max_dim, 0)));
   return reset_copies(S, st);
 }
 
@@ -1268,8 +1310,14 @@ cudaError_t GenSolver::reset_copies(const DevState& S, cudaStream_t st) {
 cudaError_t GenSolver::local(const DevState& S, int64_t begin, int64_t count, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   GK(cudaMemsetAsync(G.work, 0, sizeof(unsigned long long), st));
-  const int64_t grid = std::min<int64_t>(count, resident);
-  k_local_blocks<<<(unsigned)grid, kGenThreads, smem_bytes, st>>>(S, G, begin, count);
+  const int groups = warp_groups ? kGenThreads / 32 : 1;
+  const int64_t grid = std::min<int64_t>((count + groups - 1) / groups, resident);
+  if (warp_groups)
+    k_local_blocks<32><<<(unsigned)grid, kGenThreads, smem_bytes, st>>>(S, G, begin, count,
+                                                                       group_bytes);
+  else
+    k_local_blocks<kGenThreads><<<(unsigned)grid, kGenThreads, smem_bytes, st>>>(S, G, begin,
+                                                                                 count, group_bytes);
   return cudaGetLastError();
 }
 

@@ -65,7 +65,9 @@ struct GenSolver {
   Partition part;
   std::vector<void*> pool;
   int64_t comm_floats = 0;
-  size_t smem_bytes = 0;
+  size_t smem_bytes = 0;   // per CTA
+  size_t group_bytes = 0;  // per block (thread group)
+  bool warp_groups = false;  // a warp per block (small D) instead of a CTA
   int resident = 0;   // K1G CTAs (persistent)
   int device = 0;
 
