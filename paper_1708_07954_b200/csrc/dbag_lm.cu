@@ -5,14 +5,15 @@
 //
 // One LM iteration:
 //  - assemble (lm_solver.cpp:27-57): one thread per observation forms A = J_c,
-//    B = J_p, r and W = A^T B; U_j / g_cam_j are summed per camera (one CTA,
-//    a thread per entry, observations in input order) and V_i / g_pt_i per
-//    point, in the reference's accumulation order;
+//    B = J_p, r and W = A^T B; U_j / g_cam_j are summed per camera (one CTA:
+//    strided partial sums and a fixed-order tree) and V_i / g_pt_i per point
+//    (one thread, the reference's order);
 //  - Schur step (:59-127): V_i damped and inverted by the restated pivoted
 //    LDLT (one thread per point); the 6m x 6m complement S = U - W V^-1 W^T and
-//    its right-hand side are built by one CTA per camera block row, walking the
-//    camera's points in ascending id — the order in which the reference's point
-//    loop reaches that row — so every block sums in the reference's order;
+//    its right-hand side are built by one CTA per camera block row, whose warps
+//    own disjoint target blocks and each walk the camera's points in ascending
+//    id — the order in which the reference's point loop reaches that row — so
+//    every block sums in the reference's order, without CTA barriers;
 //  - S is factored by cuSOLVER (Cholesky; Bunch–Kaufman if S is not positive
 //    definite) — the one dense library solve, as SURVEY §8(f) plans. Eigen's
 //    blocked LDLT is not bit-pinnable, so parity is tolerance-level;
@@ -84,6 +85,16 @@ struct LmDev {
   double* S;                // [D][D] column-major (D = 6m, or 6m+3n dense)
   double* rhs;              // [D]
   double* dp;               // [3n]
+  // Schur pair lists (static): block (pair_ja[p], pair_jb[p]) gets one
+  // contribution per point both cameras observe, triplets [pair_off[p],
+  // pair_off[p+1]) of (obs in ja, obs in jb), points ascending
+  int64_t npairs;
+  const int32_t* pair_ja;
+  const int32_t* pair_jb;
+  const int64_t* pair_off;
+  const int32_t* trip_a;
+  const int32_t* trip_b;
+  const int32_t* trip_i;    // the shared point (saves a dependent load)
   double eps;
 };
 
@@ -117,26 +128,49 @@ __global__ void k_lm_jac(LmDev d, const double* pose, const double* f, const dou
     for (int b = 0; b < 3; ++b) W[3 * a + b] = A0[3 + a] * A0[b] + A1[3 + a] * A1[b];
 }
 
-// U_j (36 threads) and g_cam_j (6 threads), observations in input order.
-__global__ void k_lm_cam(LmDev d) {
+// U_j and g_cam_j (42 sums per camera): each of the CTA's 256 threads sums a
+// strided subset of the camera's observations (ascending k), then a fixed-order
+// tree. Deterministic; the order differs from the reference's sequential sum,
+// which the LM's tolerance parity (cuSOLVER) already allows.
+constexpr int kCamThreadsLm = 256;
+__global__ void __launch_bounds__(kCamThreadsLm) k_lm_cam(LmDev d) {
+  __shared__ double red[kCamThreadsLm / 32][42];
   const int j = blockIdx.x, t = threadIdx.x;
-  if (t >= 42) return;
-  double s = 0.0;
-  for (int64_t q = d.cam_off[j]; q < d.cam_off[j + 1]; ++q) {
+  double acc[42];
+#pragma unroll
+  for (int e = 0; e < 42; ++e) acc[e] = 0.0;
+  for (int64_t q = d.cam_off[j] + t; q < d.cam_off[j + 1]; q += kCamThreadsLm) {
     const int64_t k = d.cam_obs[q];
     const double* J = d.J + 18 * k;
-    if (t < 36) {
-      const int a = t / 6, b = t % 6;
-      s += J[3 + a] * J[3 + b] + J[12 + a] * J[12 + b];
-    } else {
-      const int a = t - 36;
-      s += J[3 + a] * d.r[2 * k] + J[12 + a] * d.r[2 * k + 1];
+    double c0[6], c1[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      c0[a] = J[3 + a];
+      c1[a] = J[12 + a];
+    }
+    const double r0 = d.r[2 * k], r1 = d.r[2 * k + 1];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+#pragma unroll
+      for (int b = 0; b < 6; ++b) acc[6 * a + b] += c0[a] * c0[b] + c1[a] * c1[b];
+      acc[36 + a] += c0[a] * r0 + c1[a] * r1;
     }
   }
-  if (t < 36)
-    d.U[36 * (int64_t)j + t] = s;
-  else
-    d.gc[6 * (int64_t)j + t - 36] = s;
+#pragma unroll
+  for (int e = 0; e < 42; ++e)
+    for (int off = 16; off > 0; off >>= 1) acc[e] += __shfl_down_sync(0xffffffffu, acc[e], off);
+  if ((t & 31) == 0)
+#pragma unroll
+    for (int e = 0; e < 42; ++e) red[t >> 5][e] = acc[e];
+  __syncthreads();
+  if (t < 42) {
+    double s = 0.0;
+    for (int w = 0; w < kCamThreadsLm / 32; ++w) s += red[w][t];
+    if (t < 36)
+      d.U[36 * (int64_t)j + t] = s;
+    else
+      d.gc[6 * (int64_t)j + t - 36] = s;
+  }
 }
 
 // V_i and g_pt_i, observations in input order.
@@ -267,48 +301,61 @@ __global__ void k_lm_vinv(LmDev d, double lambda) {
     d.vg[3 * i + r] = (Vi[3 * r] * g[0] + Vi[3 * r + 1] * g[1]) + Vi[3 * r + 2] * g[2];
 }
 
-// Block row ja of S and rhs (lm_solver.cpp:73-97), points in ascending id.
-constexpr int kSchurThreads = 256;
+// S and rhs (lm_solver.cpp:73-97): one warp per camera-pair block (ja, jb).
+// The block starts at U_ja damped (ja == jb) or 0 and subtracts
+// (W_a Vinv_i) W_b^T for every point i the two cameras share, in ascending i —
+// the order in which the reference's point loop reaches the block — held in
+// registers (lane e: entry e, lanes 0..3 also entries 32..35) and stored once.
+// On the diagonal block lanes 4..9 carry rhs_ja -= W_a (Vinv_i g_pt_i).
+constexpr int kSchurWarps = 8;
+constexpr int kSchurThreads = 32 * kSchurWarps;
 __global__ void __launch_bounds__(kSchurThreads) k_lm_schur(LmDev d, double lambda) {
-  __shared__ double WV[18];
-  __shared__ double rs[6];
-  const int ja = blockIdx.x;
+  const int lane = threadIdx.x & 31;
   const int64_t D = 6 * (int64_t)d.m;
-  const int t = threadIdx.x;
-  if (t < 36) {  // diagonal block: U damped
-    const int r = t / 6, c = t % 6;
-    double u = d.U[36 * (int64_t)ja + t];
-    if (r == c) u += lambda * d.U[36 * (int64_t)ja + t];
-    d.S[(6 * (int64_t)ja + c) * D + 6 * ja + r] = u;
-  }
-  if (t < 6) rs[t] = d.gc[6 * (int64_t)ja + t];
-  __syncthreads();
-  for (int64_t q = d.cam_off[ja]; q < d.cam_off[ja + 1]; ++q) {
-    const int64_t ka = d.cam_obs_p[q];
-    const int64_t i = d.pt[ka];
-    const double* Wa = d.W + 18 * ka;
-    if (t < 18) {
-      const int r = t / 3, c = t % 3;
-      const double* Vi = d.Vinv + 9 * i;
-      WV[t] = (Wa[3 * r] * Vi[c] + Wa[3 * r + 1] * Vi[3 + c]) + Wa[3 * r + 2] * Vi[6 + c];
-    } else if (t < 24) {
-      const int r = t - 18;
-      const double* vg = d.vg + 3 * i;
-      rs[r] -= (Wa[3 * r] * vg[0] + Wa[3 * r + 1] * vg[1]) + Wa[3 * r + 2] * vg[2];
+  for (int64_t p = (int64_t)blockIdx.x * kSchurWarps + (threadIdx.x >> 5); p < d.npairs;
+       p += (int64_t)gridDim.x * kSchurWarps) {
+    const int ja = d.pair_ja[p], jb = d.pair_jb[p];
+    const bool diag = ja == jb;
+    const int r0 = lane / 6, c0 = lane % 6;      // entry lane
+    const int r1 = (lane + 32) / 6, c1 = (lane + 32) % 6;  // entry lane + 32 (lanes 0..3)
+    double a0 = 0.0, a1 = 0.0, rs = 0.0;
+    if (diag) {
+      const double* U = d.U + 36 * (int64_t)ja;
+      a0 = U[lane] + (r0 == c0 ? lambda * U[lane] : 0.0);
+      if (lane < 4) a1 = U[lane + 32] + (r1 == c1 ? lambda * U[lane + 32] : 0.0);
+      if (lane >= 4 && lane < 10) rs = d.gc[6 * (int64_t)ja + lane - 4];
     }
-    __syncthreads();
-    const int64_t o0 = d.pt_off[i], no = d.pt_off[i + 1] - o0;
-    for (int64_t e = t; e < no * 36; e += kSchurThreads) {
-      const int64_t kb = d.pt_obs[o0 + e / 36];
-      const int jb = d.cam[kb];
-      const int r = (int)(e % 36) / 6, c = (int)(e % 36) % 6;
+#pragma unroll 4
+    for (int64_t t = d.pair_off[p]; t < d.pair_off[p + 1]; ++t) {
+      const int64_t ka = d.trip_a[t], kb = d.trip_b[t], i = d.trip_i[t];
+      const double* Wa = d.W + 18 * ka;
       const double* Wb = d.W + 18 * kb;
-      double* s = d.S + (6 * (int64_t)jb + c) * D + 6 * ja + r;
-      *s -= (WV[3 * r] * Wb[3 * c] + WV[3 * r + 1] * Wb[3 * c + 1]) + WV[3 * r + 2] * Wb[3 * c + 2];
+      const double* Vi = d.Vinv + 9 * i;
+      // row r of WV = Wa Vinv_i (the reference forms the 6x3 product first)
+      auto wv = [&](int r, int k) {
+        return (Wa[3 * r] * Vi[k] + Wa[3 * r + 1] * Vi[3 + k]) + Wa[3 * r + 2] * Vi[6 + k];
+      };
+      {
+        const double w0 = wv(r0, 0), w1 = wv(r0, 1), w2 = wv(r0, 2);
+        a0 -= (w0 * Wb[3 * c0] + w1 * Wb[3 * c0 + 1]) + w2 * Wb[3 * c0 + 2];
+      }
+      if (lane < 4) {
+        const double w0 = wv(r1, 0), w1 = wv(r1, 1), w2 = wv(r1, 2);
+        a1 -= (w0 * Wb[3 * c1] + w1 * Wb[3 * c1 + 1]) + w2 * Wb[3 * c1 + 2];
+      }
+      if (diag && lane >= 4 && lane < 10) {
+        const int r = lane - 4;
+        const double* g = d.gp + 3 * i;
+        const double vg0 = (Vi[0] * g[0] + Vi[1] * g[1]) + Vi[2] * g[2];
+        const double vg1 = (Vi[3] * g[0] + Vi[4] * g[1]) + Vi[5] * g[2];
+        const double vg2 = (Vi[6] * g[0] + Vi[7] * g[1]) + Vi[8] * g[2];
+        rs -= (Wa[3 * r] * vg0 + Wa[3 * r + 1] * vg1) + Wa[3 * r + 2] * vg2;
+      }
     }
-    __syncthreads();
+    d.S[(6 * (int64_t)jb + c0) * D + 6 * ja + r0] = a0;
+    if (lane < 4) d.S[(6 * (int64_t)jb + c1) * D + 6 * ja + r1] = a1;
+    if (diag && lane >= 4 && lane < 10) d.rhs[6 * (int64_t)ja + lane - 4] = rs;
   }
-  if (t < 6) d.rhs[6 * (int64_t)ja + t] = rs[t];
 }
 
 // delta_points (lm_solver.cpp:99-106) from dc.
@@ -611,7 +658,7 @@ struct dbag_lm {
     LK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, st));
     sync();
     if (hb != ~0ull) depth_error(pose, pts, (int64_t)hb);
-    k_lm_cam<<<d.m, 64, 0, st>>>(d);
+    k_lm_cam<<<d.m, kCamThreadsLm, 0, st>>>(d);
     LK(cudaGetLastError());
     k_lm_pt<<<grid_for(d.n, 128), 128, 0, st>>>(d);
     LK(cudaGetLastError());
@@ -626,7 +673,9 @@ struct dbag_lm {
       LK(cudaGetLastError());
       for (int attempt = 0; attempt < 2; ++attempt) {
         LK(cudaMemsetAsync(d.S, 0, sizeof(double) * (size_t)dim * dim, st));
-        k_lm_schur<<<m, kSchurThreads, 0, st>>>(d, lambda);
+        const int64_t blocks = std::min<int64_t>((d.npairs + kSchurWarps - 1) / kSchurWarps,
+                                                 148 * 64);
+        k_lm_schur<<<(unsigned)std::max<int64_t>(blocks, 1), kSchurThreads, 0, st>>>(d, lambda);
         LK(cudaGetLastError());
         info_fallback = false;
         if (attempt == 0) {
@@ -751,9 +800,66 @@ int dbag_lm_create(const dbag_problem_view* p, const dbag_param_view* init,
           cobs_p[fcp[p->obs_cam[k]]++] = k;
         }
     }
+    // Schur pair lists: for every point (ascending) and every ordered pair of
+    // its observations, a triplet in the list of block (cam a, cam b)
+    std::vector<int64_t> pair_id((size_t)m * m, 0);
+    for (int i = 0; i < n; ++i)
+      for (int64_t qa = po[i]; qa < po[i + 1]; ++qa)
+        for (int64_t qb = po[i]; qb < po[i + 1]; ++qb)
+          ++pair_id[(size_t)p->obs_cam[pobs[qa]] * m + p->obs_cam[pobs[qb]]];
+    std::vector<int32_t> pja, pjb;
+    std::vector<int64_t> poff(1, 0);
+    for (int ja = 0; ja < m; ++ja)
+      for (int jb = 0; jb < m; ++jb) {
+        int64_t& c = pair_id[(size_t)ja * m + jb];
+        if (c == 0) {
+          c = -1;
+          continue;
+        }
+        pja.push_back(ja);
+        pjb.push_back(jb);
+        poff.push_back(poff.back() + c);
+        c = (int64_t)pja.size() - 1;
+      }
+    std::vector<int32_t> ta(poff.back()), tb(poff.back()), ti(poff.back());
+    {
+      std::vector<int64_t> fill(poff.begin(), poff.end() - 1);
+      for (int i = 0; i < n; ++i)
+        for (int64_t qa = po[i]; qa < po[i + 1]; ++qa)
+          for (int64_t qb = po[i]; qb < po[i + 1]; ++qb) {
+            const int32_t ka = pobs[qa], kb = pobs[qb];
+            const int64_t id = pair_id[(size_t)p->obs_cam[ka] * m + p->obs_cam[kb]];
+            const int64_t pos = fill[id]++;
+            ta[pos] = ka;
+            tb[pos] = kb;
+            ti[pos] = i;
+          }
+    }
     auto up = [&](auto* dst, const void* src, size_t bytes) {
       LK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->st));
     };
+    {
+      int32_t* dja = h->alloc<int32_t>(pja.size());
+      int32_t* djb = h->alloc<int32_t>(pjb.size());
+      int64_t* dpo = h->alloc<int64_t>(poff.size());
+      int32_t* dta = h->alloc<int32_t>(ta.size());
+      int32_t* dtb = h->alloc<int32_t>(tb.size());
+      int32_t* dti = h->alloc<int32_t>(ti.size());
+      up(dja, pja.data(), 4 * pja.size());
+      up(djb, pjb.data(), 4 * pjb.size());
+      up(dpo, poff.data(), 8 * poff.size());
+      up(dta, ta.data(), 4 * ta.size());
+      up(dtb, tb.data(), 4 * tb.size());
+      up(dti, ti.data(), 4 * ti.size());
+      h->sync();  // the host vectors die at the end of this scope
+      d.npairs = (int64_t)pja.size();
+      d.pair_ja = dja;
+      d.pair_jb = djb;
+      d.pair_off = dpo;
+      d.trip_a = dta;
+      d.trip_b = dtb;
+      d.trip_i = dti;
+    }
     int32_t* dcam = h->alloc<int32_t>(l);
     int32_t* dpt = h->alloc<int32_t>(l);
     double* duv = h->alloc<double>(2 * l);
