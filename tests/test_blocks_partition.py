@@ -109,3 +109,23 @@ def test_block_size_validation(O, P):
     for bad in ((0, 1), (1, 0), (-3, 2)):
         with pytest.raises(P.ValidationError):
             P.partition(prob, *bad)
+
+
+def test_partition_fuzz_against_oracle(O, P):
+    """Random scenes and block sizes: libdbag's partition() and communication_cost()
+    equal the oracle's, bit for bit."""
+    rng = np.random.default_rng(1234)
+    for trial in range(12):
+        kw = dict(n_cameras=int(rng.integers(3, 14)), n_points=int(rng.integers(10, 60)),
+                  visibility_window=int(rng.integers(2, 6)))
+        s = scene(O, int(rng.integers(0, 10_000)), **kw)
+        prob = gpu_problem(P, s)
+        ppb, cpb = int(rng.integers(1, 40)), int(rng.integers(1, 7))
+        ob = O.AdmmSolver(s, s.cam_pose, s.cam_f, s.points, points_per_block=ppb,
+                          cameras_per_block=cpb).block_obs_ids()
+        blocks = P.partition(prob, ppb, cpb)
+        assert np.array_equal(np.concatenate([b.obs_ids for b in blocks]), ob["obs_ids"])
+        assert np.array_equal(np.concatenate([b.point_ids for b in blocks]), ob["point_ids"])
+        assert np.array_equal(np.concatenate([b.cam_ids for b in blocks]), ob["cam_ids"])
+        assert [len(b.point_ids) for b in blocks] == ob["n_points"].tolist()
+        assert P.communication_cost(prob, ppb, cpb) == s.communication_cost(ppb, cpb)

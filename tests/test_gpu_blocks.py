@@ -195,3 +195,21 @@ def test_cpp_driver_with_block_config(O, P):
         assert float(f[2]) == o["max_primal_x"] and float(f[3]) == o["max_primal_y"]
         a = float(f[1])
         assert a == o["mean_reproj_err"] or abs(a - o["mean_reproj_err"]) <= 1e-12 * abs(a)
+
+
+@pytest.mark.parametrize("config,scale,ppb,cpb,loss", [(2, 0.05, 16, 1, 0), (3, 0.02, 8, 2, 1),
+                                                       (5, 0.002, 12, 2, 0), (4, 0.005, 6, 3, 0)])
+def test_block_trajectory_config_scenes(O, P, config, scale, ppb, cpb, loss):
+    """BASELINE config scenes (scaled) with generalized blocks: 4 rounds, the state
+    trajectory bit-identical to the oracle's."""
+    sc = P.generate_config_scene(config, 0, scale)
+    p = sc.problem
+    oprob = O.Problem.create(p.cam_pose, p.cam_f, p.points, p.obs_cam, p.obs_pt, p.obs_uv)
+    osol = O.AdmmSolver(oprob, sc.init.cam_pose, p.cam_f, sc.init.points, workers=8, loss=loss,
+                        points_per_block=ppb, cameras_per_block=cpb)
+    opts = P.AdmmOptions(misfit_loss=P.LossKind(loss, 1.0), points_per_block=ppb,
+                         cameras_per_block=cpb)
+    gsol = P.AdmmSolver(p, sc.init, opts)
+    for _ in range(4):
+        assert_same_record(osol.iterate(), gsol.iterate())
+    assert_same_state(osol, gsol)
