@@ -378,6 +378,20 @@ def our_arm(args, rank, world, local_rank):
             traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
         except (OSError, ValueError, KeyError):
             traffic = None
+    # ncu-measured FP64 pipe activity of K1 (the north star's evidence for the
+    # local solves), from the committed profile of this numerics mode
+    pipe = None
+    prof = {"exact": "r1_k1_exact_jcache_config5s01.txt",
+            "fast": "r1_k1_fast_config5s01.txt"}.get(args.numerics)
+    if prof and not general and args.loss == "l2":
+        try:
+            for ln in open(os.path.join(ROOT, "profiles", prof)):
+                if ln.startswith("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"):
+                    pipe = {"frac": float(ln.split()[1]) / 100.0, "source": "profiles/" + prof,
+                            "note": "ncu --set full, config 5 at scale 0.1"}
+                    break
+        except (OSError, ValueError, IndexError):
+            pipe = None
     if dom == "local":
         roof = {"kernel": ("k_local_blocks (K1, generalized blocks, model FLOPs counted per block)"
                            if general else "k_local (K1 local solve)"), "bound": "fp64",
@@ -386,7 +400,8 @@ def our_arm(args, rank, world, local_rank):
                 "traffic_unit": "DRAM bytes per launch (ncu, profiles/r1_k1_traffic_config5.json)",
                 "peak_source": "measured on this device by dbag_measure_fp64_peak (DFMA probe); "
                                "MEASURED_PEAKS.json has no FP64 figure",
-                "hbm_frac_same_kernel": kernels["local"]["frac_hbm"]}
+                "hbm_frac_same_kernel": kernels["local"]["frac_hbm"],
+                "fp64_pipe_active_ncu": pipe}
     else:
         roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["gbs"], "peak": hbm_peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac_hbm"], "traffic": None,
