@@ -759,6 +759,8 @@ int dbag_lm_create(const dbag_problem_view* p, const dbag_param_view* init,
     const int64_t l = p->num_obs;
     if (init->num_cameras != m || init->num_points != n)
       throw LmErr{DBAG_ERR_SIZE_MISMATCH, "init state sizes do not match the problem"};
+    if (m > 16000)  // S alone would be (6m)^2 doubles = 74 GB; pair map m^2 on the host
+      throw LmErr{DBAG_ERR_UNSUPPORTED, "the dense LM camera system is limited to 16000 cameras"};
     std::string msg;
     const int vrc = validate_problem_arrays(m, n, l, p->obs_cam, p->obs_pt, p->obs_uv, p->cam_pose,
                                             p->cam_f, p->points, &msg);
