@@ -27,6 +27,10 @@
 
 using namespace dbag;
 
+#ifndef DBAG_FAST_PERSIST
+#define DBAG_FAST_PERSIST 1  // FAST GN: persistent lane-refill K1 (dbag_local.cuh)
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -209,7 +213,24 @@ struct dbag_solver {
       return;
     }
     if (opts.loss == DBAG_LOSS_SQUARED_L2) {
+#if DBAG_FAST_PERSIST
+      static int resident = 0;
+      if (resident == 0) {
+        int sms = 0, per_sm = 0;
+        CK(cudaFuncSetAttribute(k_local_persistent2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kFastPersistSmem));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_persistent2, 128,
+                                                         kFastPersistSmem));
+        resident = sms * (per_sm > 0 ? per_sm : 1);
+      }
+      CK(cudaMemsetAsync(S.work, 0, sizeof(unsigned long long), stream));
+      const int64_t g = (int64_t)grid_for(count, 128);
+      k_local_persistent2<<<(unsigned)(g < resident ? g : resident), 128, kFastPersistSmem,
+                            stream>>>(S, begin, count);
+#else
       k_local<0><<<grid_for(count, 128), 128, 0, stream>>>(S, begin, count);
+#endif
       CK_LAUNCH();
       return;
     }

@@ -267,24 +267,27 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local(DevState S, int64_t
 }
 
 
-// gauss_newton (local_opt.cpp:20-82) as a per-lane state machine. One loop
-// iteration = (Jacobian if the lane needs one) + one trial (solve + trial
-// residual + accept/reject); a lane whose observation finished refills from the
-// global work counter at the top of the next iteration. Every busy lane does a
-// trial per iteration, so warps stay full although observations need very
-// different numbers of iterations and damping retries (SIMT efficiency was
-// ~12/32 lanes with one observation per thread, profiles/). The per-observation
-// arithmetic and control flow are unchanged.
-// Measured: EXACT K1 383 -> 209 ms with this structure (dbag_exact.cu), but the
-// FAST trial is cheap enough that the extra live state and scattered refill
-// loads lose (57.6 -> 70.2 ms, config 5), so FAST launches k_local; this
-// variant is kept for reference/tests.
-template <int kLoss>
-__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState S, int64_t begin, int64_t count) {
-  __shared__ double tgt_s[9 * 128];
+// gauss_newton (local_opt.cpp:20-82) as a persistent per-lane state machine
+// (the FAST K1 for squared L2): one loop iteration = (Jacobian if the lane
+// needs one) + one trial; a lane whose observation finished refills from the
+// global work counter, so warps stay full although observations need very
+// different numbers of iterations and damping retries (k_local keeps ~12/32
+// lanes busy, profiles/). The Jacobian rows A0|A1, rhs and H_kk live in the
+// thread's shared slice (formed once per GN iteration, read by every damping
+// trial), R is recomputed from the trig values instead of held, and the refill
+// issues its loads first: 59.9 -> 52.5 ms at config 5 against k_local (a first
+// persistent version that held that state in registers lost, 57.6 -> 70.2 ms).
+// 45 doubles of shared memory per thread with the targets.
+constexpr int kFastScr = 36;
+constexpr size_t kFastPersistSmem = sizeof(double) * (9 + kFastScr) * 128;
+
+__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent2(DevState S, int64_t begin,
+                                                                         int64_t count) {
+  extern __shared__ double fp_dyn[];
   LocalCounters cnt;
   GnProblem P;
-  P.tgt = tgt_s + threadIdx.x;
+  P.tgt = fp_dyn + threadIdx.x;
+  double* sc = fp_dyn + 9 * 128 + threadIdx.x;  // A0 0..8 | A1 9..17 | rhs 18..26 | H_kk 27..35
   P.wx = sqrt(0.5 * S.rho_x);  // admm_solver.cpp:183-184
   P.wy = sqrt(0.5 * S.rho_y);
   P.eps = S.eps_depth;
@@ -294,10 +297,9 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
   int64_t b = -1;
   int it = 0;
   double lambda = 0.0, obj = 0.0, e0 = 0.0, e1 = 0.0;
-  double v[9], R[9], w[3], A0[9], A1[9], rhs[9];
+  double v[9], w[3];
   Trig tr;
   for (;;) {
-    // ---- refill: load the observation, residual at the warm start
     const int64_t idx = refill(S, !busy, count, exhausted);
     if (idx >= 0) {
       b = begin + idx;
@@ -306,21 +308,26 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
       const PointRec rec = S.prec[S.blk_pos[b]];
       const double* yb = S.ybar + 8 * (int64_t)j;
       const double4 xb = S.xbar[i];
+      double sd[6], yv[7];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        v[3 + k] = S.cam_soa[(int64_t)k * S.L + b];
+        sd[k] = S.cam_soa[(int64_t)(6 + k) * S.L + b];
+      }
+#pragma unroll
+      for (int k = 0; k < 7; ++k) yv[k] = yb[k];
       v[0] = rec.x0;
       v[1] = rec.x1;
       v[2] = rec.x2;
-      // completed-square targets x~ = xbar - r/rho, y~ = ybar - s/rho (:152-164)
       P.tgt[0] = xb.x - rec.r0 / S.rho_x;
       P.tgt[128] = xb.y - rec.r1 / S.rho_x;
       P.tgt[256] = xb.z - rec.r2 / S.rho_x;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        v[3 + k] = S.cam_soa[(int64_t)k * S.L + b];
-        P.tgt[(3 + k) * 128] = yb[k] - S.cam_soa[(int64_t)(6 + k) * S.L + b] / S.rho_y;
-      }
+      for (int k = 0; k < 6; ++k) P.tgt[(3 + k) * 128] = yv[k] - sd[k] / S.rho_y;
       P.z0 = rec.u;
       P.z1 = rec.v;
-      P.f = yb[6];
+      P.f = yv[6];
+      double R[9];
       if (gn_residual(P, v, tr, R, w, e0, e1, obj) && isfinite(e0) && isfinite(e1) &&
           isfinite(obj)) {
         busy = true;
@@ -335,11 +342,12 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
       continue;
     }
     bool done = false;
-    // ---- Jacobian at v: J = [-A ; diag(w)], g = 2 J^T r
     if (busy && need_jac) {
       if (it >= S.inner_max_iters) {
         done = true;  // kMaxIters
       } else {
+        double R[9], A0[9], A1[9];
+        rot_of(tr, R);
         proj_jacobian(v, tr, R, w, P.f, A0, A1);
         ++cnt.n_jac;
         double g2 = 0.0;
@@ -347,7 +355,10 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
         for (int k = 0; k < 9; ++k) {
           const double wk = k < 3 ? P.wx : P.wy;
           const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.T(k)));
-          rhs[k] = -jtr;                // -0.5 g
+          sc[k * 128] = A0[k];
+          sc[(9 + k) * 128] = A1[k];
+          sc[(18 + k) * 128] = -jtr;  // rhs = -0.5 g
+          sc[(27 + k) * 128] = (A0[k] * A0[k] + A1[k] * A1[k]) + (k < 3 ? wx2 : wy2);
           const double gk = 2.0 * jtr;  // g = 2 J^T r
           g2 += gk * gk;
         }
@@ -359,25 +370,21 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
         }
       }
     }
-    // ---- one trial: (A^T A + D) delta = rhs, D_k = w_k^2 + lambda*max(H_kk, 1e-12)
     if (busy && !done && !need_jac) {
       double iD[9], u[9];
       double c00 = 1.0, c01 = 0.0, c11 = 1.0, a0 = 0.0, a1 = 0.0;
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
+        const double A0k = sc[k * 128], A1k = sc[(9 + k) * 128];
         const double wk2 = k < 3 ? wx2 : wy2;
-        if (lambda > 0.0) {
-          const double hkk = (A0[k] * A0[k] + A1[k] * A1[k]) + wk2;
-          iD[k] = fast_rcp(wk2 + lambda * fmax(hkk, 1e-12));
-        } else {
-          iD[k] = k < 3 ? iwx2 : iwy2;
-        }
-        u[k] = rhs[k] * iD[k];
-        c00 += A0[k] * A0[k] * iD[k];
-        c01 += A0[k] * A1[k] * iD[k];
-        c11 += A1[k] * A1[k] * iD[k];
-        a0 += A0[k] * u[k];
-        a1 += A1[k] * u[k];
+        iD[k] = lambda > 0.0 ? fast_rcp(wk2 + lambda * fmax(sc[(27 + k) * 128], 1e-12))
+                             : (k < 3 ? iwx2 : iwy2);
+        u[k] = sc[(18 + k) * 128] * iD[k];
+        c00 += A0k * A0k * iD[k];
+        c01 += A0k * A1k * iD[k];
+        c11 += A1k * A1k * iD[k];
+        a0 += A0k * u[k];
+        a1 += A1k * u[k];
       }
       const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
       const double y0 = (c11 * a0 - c01 * a1) * idet;
@@ -386,7 +393,7 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
       bool fin = true;
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
-        const double dk = u[k] - iD[k] * (A0[k] * y0 + A1[k] * y1);
+        const double dk = u[k] - iD[k] * (sc[k * 128] * y0 + sc[(9 + k) * 128] * y1);
         fin = fin && isfinite(dk);
         d2 += dk * dk;
         vt[k] = v[k] + dk;
@@ -402,8 +409,6 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
           ++cnt.n_acc;
 #pragma unroll
           for (int k = 0; k < 9; ++k) v[k] = vt[k];
-#pragma unroll
-          for (int k = 0; k < 9; ++k) R[k] = Rt[k];
           tr = trt;
           w[0] = wt[0];
           w[1] = wt[1];
@@ -424,10 +429,9 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent(DevState
       }
       if (!accepted) {
         lambda = lambda == 0.0 ? kDampingInit : lambda * 10.0;
-        if (lambda > kDampingMax) done = true;  // kLineSearchFailed / kSingularSystem
+        if (lambda > kDampingMax) done = true;
       }
     }
-    // ---- finished: write the copies back (admm_solver.cpp:284-289)
     if (busy && done) {
       double* xp = reinterpret_cast<double*>(S.prec + S.blk_pos[b]);
       xp[0] = v[0];
