@@ -372,8 +372,6 @@ struct dbag_solver {
     else
       k_reproj_blocks<2><<<parts, 256, 0, stream>>>(S);
     CK_LAUNCH();
-    double* d_out = S.record + kRecFields - 1;  // scratch: reuse after the record fields
-    (void)d_out;
     k_sum_parts<<<1, 1024, 0, stream>>>(S, parts, S.record + kRecFields);
     CK_LAUNCH();
     double sum = 0.0;
