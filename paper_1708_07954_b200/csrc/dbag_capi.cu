@@ -27,6 +27,9 @@
 
 using namespace dbag;
 
+#ifndef DBAG_EFFORT_ORDER
+#define DBAG_EFFORT_ORDER 1  // Huber K1 in last-round effort order (launch_local)
+#endif
 #ifndef DBAG_FAST_PERSIST
 #define DBAG_FAST_PERSIST 1  // FAST GN: persistent lane-refill K1 (dbag_local.cuh)
 #endif
@@ -80,6 +83,11 @@ int guarded(F&& f) {
 }
 
 [[noreturn]] void raise(int code, const std::string& msg) { throw StatusError{code, msg}; }
+
+__global__ void k_iota(int64_t n, int32_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int32_t)i;
+}
 
 }  // namespace
 
@@ -139,6 +147,12 @@ struct dbag_solver {
   bool sharded() const { return world > 1; }
   // generalized blocks (BlockConfig != {1,1}); null for (1,1)
   std::unique_ptr<blocks::GenSolver> gen;
+  // effort-ordered Huber K1 buffers (see effort_order)
+  int32_t* order_buf = nullptr;
+  int32_t* order_iota = nullptr;
+  uint16_t* effort_sorted = nullptr;
+  void* order_tmp = nullptr;
+  size_t order_tmp_bytes = 0;
   int64_t num_blocks() const { return gen ? gen->G.B : S.L; }
 
   ~dbag_solver() {
@@ -209,7 +223,8 @@ struct dbag_solver {
       return;
     }
     if (exact()) {
-      CK(exact::launch_local(S, begin, count, stream));
+      CK(exact::launch_local(opts.loss == DBAG_LOSS_HUBER ? effort_order(begin, count) : S, begin,
+                             count, stream));
       return;
     }
     if (opts.loss == DBAG_LOSS_SQUARED_L2) {
@@ -234,8 +249,24 @@ struct dbag_solver {
       CK_LAUNCH();
       return;
     }
-    k_local_huber<<<grid_for(count, kHuberThreads), kHuberThreads, 0, stream>>>(S, begin, count);
+    const DevState So = effort_order(begin, count);
+    k_local_huber<<<grid_for(count, kHuberThreads), kHuberThreads, 0, stream>>>(So, begin, count);
     CK_LAUNCH();
+  }
+
+  // Huber K1 over all blocks: process the observations in ascending order of
+  // their last local solve's value evaluations (stable radix sort, block order
+  // within ties), so a warp holds solves of similar length. Observations are
+  // independent, so results are unchanged; the sort is inside the round.
+  DevState effort_order(int64_t begin, int64_t count) {
+    DevState So = S;
+    So.order = nullptr;
+    if (S.effort && begin == 0 && count == S.L && S.L > 0) {
+      CK(cub::DeviceRadixSort::SortPairs(order_tmp, order_tmp_bytes, S.effort, effort_sorted,
+                                         order_iota, order_buf, (int)S.L, 0, 16, stream));
+      So.order = order_buf;
+    }
+    return So;
   }
 
   void reset_err() { CK(cudaMemsetAsync(S.err_block, 0xff, sizeof(int64_t), stream)); }
@@ -542,6 +573,22 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     S.record = dev_alloc<double>(pool, kRecFields + 4);
     S.metric_part = dev_alloc<double>(pool, kRecFields);
     S.work = dev_alloc<unsigned long long>(pool, 1);
+    S.effort = nullptr;
+    S.order = nullptr;
+    if (opts->loss == DBAG_LOSS_HUBER && DBAG_EFFORT_ORDER) {
+      // effort-ordered Huber K1 (launch_local): per-observation effort, the
+      // order it sorts into, and the sort's buffers
+      S.effort = dev_alloc<uint16_t>(pool, L);
+      CK(cudaMemsetAsync(S.effort, 0, sizeof(uint16_t) * (size_t)L, st));
+      h->order_buf = dev_alloc<int32_t>(pool, L);
+      h->order_iota = dev_alloc<int32_t>(pool, L);
+      h->effort_sorted = dev_alloc<uint16_t>(pool, L);
+      k_iota<<<grid_for(L, 256), 256, 0, st>>>(L, h->order_iota);
+      CK_LAUNCH();
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, h->order_tmp_bytes, S.effort, h->effort_sorted,
+                                         h->order_iota, h->order_buf, (int)L, 0, 16, st));
+      h->order_tmp = dev_alloc<char>(pool, h->order_tmp_bytes);
+    }
 
     S.world = 1;
     S.rank = 0;

@@ -56,6 +56,10 @@ struct DevState {
   double* record;         // DevRecord
   double* metric_part;    // [kRecFields] this rank's partial record (raw sums)
   unsigned long long* work;  // K1 work counter (zeroed before each launch)
+  // effort-ordered Huber K1: value evaluations of each observation's last local
+  // solve, and the processing order the next full launch uses (null: block order)
+  uint16_t* effort;   // [L]
+  const int32_t* order;  // [L] or null
   // ---- multi-GPU shard (null/0 on a single-GPU solver) ----
   int32_t world, rank;
   int32_t* bp_of_local;   // [N] global boundary index of a local point, or -1

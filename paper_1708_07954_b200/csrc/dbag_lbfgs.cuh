@@ -209,9 +209,10 @@ __device__ __noinline__ bool local_lbfgs(const DevState& S, const HuberProblem& 
 
 __global__ void __launch_bounds__(kHuberThreads) k_local_huber(DevState S, int64_t begin,
                                                                int64_t count) {
-  const int64_t b = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   LocalCounters cnt;
-  if (b < begin + count) {
+  if (tix < count) {
+    const int64_t b = S.order ? (int64_t)S.order[tix] : begin + tix;  // effort order (full launch)
     const int32_t j = S.blk_cam[b];
     const int32_t i = S.blk_pt[b];
     const int32_t p = S.blk_pos[b];
@@ -242,7 +243,10 @@ __global__ void __launch_bounds__(kHuberThreads) k_local_huber(DevState S, int64
     P.rho_x = S.rho_x;
     P.rho_y = S.rho_y;
     P.eps = S.eps_depth;
-    if (!local_lbfgs(S, P, v, cnt)) {
+    const unsigned nv0 = cnt.n_trial;
+    const bool solved = local_lbfgs(S, P, v, cnt);
+    if (S.effort) S.effort[b] = (uint16_t)min(cnt.n_trial - nv0, 65535u);
+    if (!solved) {
       atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)b);
     } else {
       double* xp = reinterpret_cast<double*>(S.prec + p);
