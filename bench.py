@@ -435,7 +435,9 @@ def our_arm(args, rank, world, local_rank):
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu,
             "other_numerics": other_line,
             "clocks": clocks.summary(),
-            "gpu_launches": (6 if world > 1 else 4) * args.steps,
+            # our kernels per round: K1, K3, K2, k_final, k_combine (+ k_pack_send when
+            # sharded); the Huber effort-order sort adds CUB's radix-sort kernels
+            "gpu_launches": (6 if world > 1 else 5) * args.steps,
             "counters": {k: stats[k] for k in ("n_jacobian", "n_trial", "n_accept",
                                                "n_direction", "n_pairs_used")},
             "last_round": {k: last[k] for k in ("iter", "mean_reproj_err", "max_primal_x",
