@@ -84,6 +84,15 @@ int guarded(F&& f) {
 
 [[noreturn]] void raise(int code, const std::string& msg) { throw StatusError{code, msg}; }
 
+__global__ void k_pack_xbar(int32_t n, const double4* x, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 v = x[i];
+  out[3 * i] = v.x;
+  out[3 * i + 1] = v.y;
+  out[3 * i + 2] = v.z;
+}
+
 __global__ void k_iota(int64_t n, int32_t* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (int32_t)i;
@@ -148,6 +157,7 @@ struct dbag_solver {
   // generalized blocks (BlockConfig != {1,1}); null for (1,1)
   std::unique_ptr<blocks::GenSolver> gen;
   // effort-ordered Huber K1 buffers (see effort_order)
+  double* pack_pts = nullptr;  // [n][3] device staging for dbag_get_consensus
   int32_t* order_buf = nullptr;
   int32_t* order_iota = nullptr;
   uint16_t* effort_sorted = nullptr;
@@ -1015,9 +1025,24 @@ int dbag_get_consensus(dbag_solver* h, double* cam_pose, double* cam_f, double* 
     CK(cudaSetDevice(h->device));
     const DevState& S = h->S;
     std::vector<double> y(8 * (size_t)S.M);
-    std::vector<double4> x(S.N);
     CK(cudaMemcpyAsync(y.data(), S.ybar, sizeof(double) * y.size(), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(x.data(), S.xbar, sizeof(double4) * x.size(), cudaMemcpyDeviceToHost, h->stream));
+    if (!h->sharded()) {
+      // points: packed to [n][3] on the device, one copy into the caller's buffer
+      if (!h->pack_pts) h->pack_pts = dev_alloc<double>(h->pool, 3 * (size_t)S.N);
+      k_pack_xbar<<<grid_for(S.N, 256), 256, 0, h->stream>>>(S.N, S.xbar, h->pack_pts);
+      CK_LAUNCH();
+      CK(cudaMemcpyAsync(points, h->pack_pts, sizeof(double) * 3 * (size_t)S.N,
+                         cudaMemcpyDeviceToHost, h->stream));
+      h->sync();
+      for (int j = 0; j < S.M; ++j) {
+        for (int k = 0; k < 6; ++k) cam_pose[6 * (size_t)j + k] = y[8 * (size_t)j + k];
+        if (cam_f) cam_f[j] = y[8 * (size_t)j + 6];
+      }
+      return;
+    }
+    std::unique_ptr<double4[]> x(new double4[S.N]);
+    CK(cudaMemcpyAsync(x.get(), S.xbar, sizeof(double4) * (size_t)S.N, cudaMemcpyDeviceToHost,
+                       h->stream));
     h->sync();
     // a shard writes its own cameras/points at their global indices
     for (int j = 0; j < S.M; ++j) {
