@@ -51,14 +51,22 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in _inputs() if os.path.exists(f))
 
 
-def build(force=False, verbose=False, extra=()):
+def build(force=False, verbose=False, extra=(), only=None):
+    """only: recompile just these sources (with `extra`) into a scratch object
+    dir and link them with the main build's objects (variant A/B builds)."""
     if not force and up_to_date():
         return LIB
     objdir = os.path.join(HERE, "_obj")
     os.makedirs(objdir, exist_ok=True)
+    vardir = os.path.join(HERE, "_obj_var")
     objs = []
     for src, flags in SOURCES:
-        obj = os.path.join(objdir, src + ".o")
+        if only is not None and src not in only:
+            objs.append(os.path.join(objdir, src + ".o"))
+            continue
+        if only is not None:
+            os.makedirs(vardir, exist_ok=True)
+        obj = os.path.join(vardir if only is not None else objdir, src + ".o")
         cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", *flags, *extra, "-c",
                os.path.join(CSRC, src), "-o", obj]

@@ -17,6 +17,12 @@ VARIANTS = {
     "exact_minb4": ["-DDBAG_K1E_MINB=4"],
     "jcache0": ["-DDBAG_K1E_JCACHE=0"],
     "jcache1": ["-DDBAG_K1E_JCACHE=1"],
+    "smstate0": ["-DDBAG_K1E_SMSTATE=0"],
+    "smstate1": ["-DDBAG_K1E_SMSTATE=1"],
+    "abl_pivot": ["-DDBAG_ABLATE_PIVOT"],
+    "fastpiv0": ["-DDBAG_K1E_FASTPIV=0"],
+    "fastpiv1": ["-DDBAG_K1E_FASTPIV=1"],
+    "packord0": ["-DDBAG_K1E_PACKORD=0"],
 }
 
 
@@ -26,7 +32,7 @@ def main(names):
     saved = b.LIB
     for n in names or VARIANTS:
         b.LIB = os.path.join(out, n + ".so")
-        b.build(force=True, extra=VARIANTS[n])
+        b.build(force=True, extra=VARIANTS[n], only=["dbag_exact.cu"])
         print("built", b.LIB)
     b.LIB = saved
 
