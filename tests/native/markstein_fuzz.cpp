@@ -9,15 +9,15 @@
 
 static inline bool safe(double a, double b) {  // same guard as the device code
   const double aa = std::fabs(a), ab = std::fabs(b);
-  return aa < 0x1p+900 && ab < 0x1p+900 && aa > 0x1p-900 && ab > 0x1p-900;
+  return (aa == 0.0 || (aa >= 0x1p-400 && aa <= 0x1p+400)) && ab >= 0x1p-400 && ab <= 0x1p+400;
 }
 static inline double mdiv(double a, double b, double y) {
-  // the device's qdiv_run: zero numerators take a*y (IEEE zero sign)
-  if (a == 0.0 && std::fabs(b) < 0x1p+900 && std::fabs(b) > 0x1p-900) return a * y;
+  // the device's column division: zero numerators take a*y (IEEE zero sign)
   if (!safe(a, b)) return a / b;
   const double q0 = a * y;
   const double r = std::fma(-q0, b, a);
-  return std::fma(r, y, q0);
+  const double q = std::fma(r, y, q0);
+  return a == 0.0 ? q0 : q;  // dbag_exact.cu ldlt_col (MDIV)
 }
 static inline double bits(uint64_t u) { double d; std::memcpy(&d, &u, 8); return d; }
 
@@ -36,7 +36,8 @@ int main(int argc, char** argv) {
   };
   for (long long i = 0; i < N; ++i) {
     // random bit patterns in a wide exponent band
-    const uint64_t ea = 1023 - 200 + g() % 400, eb = 1023 - 200 + g() % 400;
+    // the whole guarded band [2^-400, 2^400] and a little beyond it
+    const uint64_t ea = 1023 - 410 + g() % 821, eb = 1023 - 410 + g() % 821;
     const uint64_t ma = g() & ((1ull << 52) - 1), mb = g() & ((1ull << 52) - 1);
     double a = bits((ea << 52) | ma), b = bits((eb << 52) | mb);
     if (g() & 1) a = -a;

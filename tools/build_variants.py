@@ -23,6 +23,16 @@ VARIANTS = {
     "fastpiv0": ["-DDBAG_K1E_FASTPIV=0"],
     "fastpiv1": ["-DDBAG_K1E_FASTPIV=1"],
     "packord0": ["-DDBAG_K1E_PACKORD=0"],
+    "mdiv0": ["-DDBAG_K1E_MDIV=0"],
+    "mdiv1": ["-DDBAG_K1E_MDIV=1"],
+    "pivcall0": ["-DDBAG_K1E_PIVCALL=0"],
+    "pivcall1": ["-DDBAG_K1E_PIVCALL=1"],
+    "sincoscall": ["-DDBAG_SINCOS_CALL=1"],
+    "sync128": ["-DDBAG_K1E_SYNC=1"],
+    "sync384": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_THREADS=384"],
+    "t384": ["-DDBAG_K1E_THREADS=384"],
+    "sync128_mdiv1": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_MDIV=1"],
+    "sync256": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_THREADS=64"],
 }
 
 
