@@ -32,6 +32,9 @@ VARIANTS = {
     "sync384": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_THREADS=384"],
     "t384": ["-DDBAG_K1E_THREADS=384"],
     "sync128_mdiv1": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_MDIV=1"],
+    "unified0": ["-DDBAG_K1E_UNIFIED=0"],
+    "unified1": ["-DDBAG_K1E_UNIFIED=1"],
+    "unified1_mdiv1": ["-DDBAG_K1E_UNIFIED=1", "-DDBAG_K1E_MDIV=1"],
     "sync256": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_THREADS=64"],
 }
 
