@@ -104,6 +104,20 @@ __device__ __forceinline__ void edrot_x(const ETrig& t, const double* x, double 
   vG[2] = 0.0;
 }
 
+// try_project (geometry.cpp:92-99) given the trig values t of v's angles.
+__device__ __forceinline__ bool eproject_t(const double v[9], double f, double eps,
+                                           const ETrig& t, double R[9], double w[3],
+                                           double z[2]) {
+  erot(t, R);
+  w[0] = row3(R, v) + v[6];
+  w[1] = row3(R + 3, v) + v[7];
+  w[2] = row3(R + 6, v) + v[8];
+  if (!(w[2] >= eps)) return false;
+  z[0] = f * w[0] / w[2];  // geometry.cpp:98
+  z[1] = f * w[1] / w[2];
+  return true;
+}
+
 // try_project (geometry.cpp:92-99): w = R x + t.
 __device__ __forceinline__ bool eproject(const double v[9], double f, double eps, ETrig& t,
                                          double R[9], double w[3], double z[2]) {

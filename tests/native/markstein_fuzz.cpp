@@ -9,15 +9,15 @@
 
 static inline bool safe(double a, double b) {  // same guard as the device code
   const double aa = std::fabs(a), ab = std::fabs(b);
-  return (aa == 0.0 || (aa >= 0x1p-400 && aa <= 0x1p+400)) && ab >= 0x1p-400 && ab <= 0x1p+400;
+  return aa >= 0x1p-400 && aa < 0x1p+400 && ab >= 0x1p-400 && ab < 0x1p+400;
 }
 static inline double mdiv(double a, double b, double y) {
-  // the device's column division: zero numerators take a*y (IEEE zero sign)
+  // dbag_exact.cu ldlt_col (MD): zeros, denormals, huge values, NaN and inf
+  // leave the guarded exponent band and take IEEE '/' (the out-of-line solve)
   if (!safe(a, b)) return a / b;
   const double q0 = a * y;
   const double r = std::fma(-q0, b, a);
-  const double q = std::fma(r, y, q0);
-  return a == 0.0 ? q0 : q;  // dbag_exact.cu ldlt_col (MDIV)
+  return std::fma(r, y, q0);
 }
 static inline double bits(uint64_t u) { double d; std::memcpy(&d, &u, 8); return d; }
 

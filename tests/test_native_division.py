@@ -1,8 +1,9 @@
 """Markstein division (a shared correctly rounded reciprocal plus one FMA
-correction) against IEEE '/': the identity behind the shared-reciprocal LDLT
-variants recorded in DESIGN.md §4 (bit-identical, measured slower, not
-shipped). This fuzz checks bit-identity with '/' (including the sign of zero)
-on random, adversarial and LDLT-like operands, compiled with hardware FMA."""
+correction) against IEEE '/': the identity behind the EXACT K1's LDLT column
+divisions (dbag_exact.cu ldlt_col). This fuzz checks bit-identity
+with '/' on random (the whole guarded exponent band and beyond), adversarial
+and LDLT-like operands, compiled with hardware FMA; operands outside the band
+take '/' as on the device."""
 import os
 import subprocess
 

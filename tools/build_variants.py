@@ -35,6 +35,11 @@ VARIANTS = {
     "unified0": ["-DDBAG_K1E_UNIFIED=0"],
     "unified1": ["-DDBAG_K1E_UNIFIED=1"],
     "unified1_mdiv1": ["-DDBAG_K1E_UNIFIED=1", "-DDBAG_K1E_MDIV=1"],
+    "roll0": ["-DDBAG_K1E_ROLLTGT=0", "-DDBAG_K1E_ROLLTRIG=0"],
+    "roll1": [],
+    "roll1_mdiv1": ["-DDBAG_K1E_MDIV=1"],
+    "mdiv0": ["-DDBAG_K1E_MDIV=0"],
+    "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "sync256": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_THREADS=64"],
 }
 
