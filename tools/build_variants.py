@@ -25,6 +25,10 @@ VARIANTS = {
     "packord0": ["-DDBAG_K1E_PACKORD=0"],
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
+    "cur": [],
+    "nosync": ["-DDBAG_K1E_SYNC=0"],
+    "mdsolve0": ["-DDBAG_K1E_MDSOLVE=0"],
+    "mdtgt0": ["-DDBAG_K1E_MDTGT=0"],
     "pivcall0": ["-DDBAG_K1E_PIVCALL=0"],
     "pivcall1": ["-DDBAG_K1E_PIVCALL=1"],
     "sincoscall": ["-DDBAG_SINCOS_CALL=1"],
@@ -40,6 +44,10 @@ VARIANTS = {
     "roll1_mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
+    "cur": [],
+    "nosync": ["-DDBAG_K1E_SYNC=0"],
+    "mdsolve0": ["-DDBAG_K1E_MDSOLVE=0"],
+    "mdtgt0": ["-DDBAG_K1E_MDTGT=0"],
     "sync256": ["-DDBAG_K1E_SYNC=1", "-DDBAG_K1E_THREADS=64"],
 }
 
