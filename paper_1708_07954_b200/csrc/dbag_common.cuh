@@ -94,6 +94,48 @@ __device__ __forceinline__ int64_t refill(const DevState& S, bool idle, int64_t 
   return idx < (unsigned long long)count ? (int64_t)idx : -1;
 }
 
+// refill() with a warp-local queue [q0, q1) of claimed indices: one global
+// atomic per kBatch observations instead of one per refill. Every index is
+// still taken exactly once; lanes take queue entries in lane order.
+struct WarpQueue {
+  unsigned long long q0 = 0, q1 = 0;  // warp-uniform
+  bool end = false;                   // a claim reached `count`
+};
+template <int kBatch>
+__device__ __forceinline__ int64_t refill_batched(const DevState& S, bool idle, int64_t count,
+                                                  bool& exhausted, WarpQueue& q) {
+  const unsigned full = 0xffffffffu;
+  const unsigned m = __ballot_sync(full, idle && !exhausted);
+  if (m == 0) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  const unsigned n = __popc(m);
+  const unsigned rank = __popc(m & ((1u << lane) - 1u));
+  const unsigned long long r = q.q1 - q.q0;
+  unsigned long long idx;
+  if (r >= n) {
+    idx = q.q0 + rank;
+    q.q0 += n;
+  } else {
+    const unsigned need = n - (unsigned)r;
+    const unsigned want = need > (unsigned)kBatch ? need : (unsigned)kBatch;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(S.work, (unsigned long long)want);
+    base = __shfl_sync(full, base, leader);
+    idx = rank < r ? q.q0 + rank : base + (rank - r);
+    q.q0 = base + need;
+    q.q1 = base + want;
+    if (q.q1 >= (unsigned long long)count) {
+      q.end = true;
+      q.q1 = (unsigned long long)count;
+      if (q.q0 > q.q1) q.q0 = q.q1;
+    }
+  }
+  if (q.end && q.q0 >= q.q1) exhausted = true;
+  if (!(m & (1u << lane))) return -1;
+  return idx < (unsigned long long)count ? (int64_t)idx : -1;
+}
+
 // DevRecord layout (doubles)
 enum RecField {
   kRecSumErr = 0, kRecMaxPx, kRecMaxPy, kRecMaxDx, kRecMaxDy, kRecInfeasible, kRecCamMse,

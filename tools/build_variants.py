@@ -26,6 +26,8 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "batch0": ["-DDBAG_K1E_BATCH=0"],
+    "batch64": ["-DDBAG_K1E_BATCH=64"],
     "nosync": ["-DDBAG_K1E_SYNC=0"],
     "mdsolve0": ["-DDBAG_K1E_MDSOLVE=0"],
     "mdtgt0": ["-DDBAG_K1E_MDTGT=0"],
@@ -45,6 +47,8 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "batch0": ["-DDBAG_K1E_BATCH=0"],
+    "batch64": ["-DDBAG_K1E_BATCH=64"],
     "nosync": ["-DDBAG_K1E_SYNC=0"],
     "mdsolve0": ["-DDBAG_K1E_MDSOLVE=0"],
     "mdtgt0": ["-DDBAG_K1E_MDTGT=0"],
