@@ -101,9 +101,38 @@ struct WarpQueue {
   unsigned long long q0 = 0, q1 = 0;  // warp-uniform
   bool end = false;                   // a claim reached `count`
 };
-template <int kBatch>
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// When a batch [base, base + n) is claimed, pull its observations' scattered
+// lines (point record, point consensus) and its camera-SoA rows into L2, so
+// the refills that consume the batch over the next iterations hit L2.
+__device__ __forceinline__ void prefetch_batch(const DevState& S, int64_t begin,
+                                               unsigned long long base, unsigned n,
+                                               int64_t count) {
+  const int lane = threadIdx.x & 31;
+  for (unsigned k = lane; k < n; k += 32) {
+    const unsigned long long e = base + k;
+    if (e < (unsigned long long)count) {
+      const int64_t b = begin + (int64_t)e;
+      prefetch_l2(S.prec + S.blk_pos[b]);
+      prefetch_l2(S.xbar + S.blk_pt[b]);
+    }
+  }
+  // 12 SoA rows of the batch: 8 B per observation, 128 B lines
+  const unsigned lines = (n + 15) / 16;
+  for (unsigned k = lane; k < 12 * lines; k += 32) {
+    const unsigned row = k / lines, ln = k % lines;
+    const unsigned long long e = base + 16ull * ln;
+    if (e < (unsigned long long)count) prefetch_l2(S.cam_soa + (int64_t)row * S.L + begin + (int64_t)e);
+  }
+}
+
+template <int kBatch, bool kPrefetch = false>
 __device__ __forceinline__ int64_t refill_batched(const DevState& S, bool idle, int64_t count,
-                                                  bool& exhausted, WarpQueue& q) {
+                                                  bool& exhausted, WarpQueue& q,
+                                                  int64_t begin = 0) {
   const unsigned full = 0xffffffffu;
   const unsigned m = __ballot_sync(full, idle && !exhausted);
   if (m == 0) return -1;
@@ -122,6 +151,7 @@ __device__ __forceinline__ int64_t refill_batched(const DevState& S, bool idle, 
     unsigned long long base = 0;
     if (lane == leader) base = atomicAdd(S.work, (unsigned long long)want);
     base = __shfl_sync(full, base, leader);
+    if (kPrefetch) prefetch_batch(S, begin, base + need, want - need, count);
     idx = rank < r ? q.q0 + rank : base + (rank - r);
     q.q0 = base + need;
     q.q1 = base + want;

@@ -27,6 +27,8 @@ VARIANTS = {
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
+    "pf0": ["-DDBAG_K1E_PREFETCH=0"],
+    "pf0_sync0": ["-DDBAG_K1E_PREFETCH=0", "-DDBAG_K1E_SYNC=0"],
     "batch64": ["-DDBAG_K1E_BATCH=64"],
     "nosync": ["-DDBAG_K1E_SYNC=0"],
     "mdsolve0": ["-DDBAG_K1E_MDSOLVE=0"],
@@ -48,6 +50,8 @@ VARIANTS = {
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
+    "pf0": ["-DDBAG_K1E_PREFETCH=0"],
+    "pf0_sync0": ["-DDBAG_K1E_PREFETCH=0", "-DDBAG_K1E_SYNC=0"],
     "batch64": ["-DDBAG_K1E_BATCH=64"],
     "nosync": ["-DDBAG_K1E_SYNC=0"],
     "mdsolve0": ["-DDBAG_K1E_MDSOLVE=0"],
