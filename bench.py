@@ -381,7 +381,7 @@ def our_arm(args, rank, world, local_rank):
     # ncu-measured FP64 pipe activity of K1 (the north star's evidence for the
     # local solves), from the committed profile of this numerics mode
     pipe = None
-    prof = {"exact": "r1_k1_exact_jcache_config5s01.txt",
+    prof = {"exact": "r1_k1_exact_markstein_config5s01.txt",
             "fast": "r1_k1_fast_config5s01.txt"}.get(args.numerics)
     if prof and not general and args.loss == "l2":
         try:
