@@ -607,6 +607,8 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     const dbag_options& o = *opts;
     S.rho_x = o.rho_x;
     S.rho_y = o.rho_y;
+    S.w_x = std::sqrt(0.5 * o.rho_x);  // IEEE sqrt: the device's sqrt() bit for bit
+    S.w_y = std::sqrt(0.5 * o.rho_y);
     S.eps_depth = o.eps_depth;
     S.huber_delta = o.huber_delta;
     S.grad_tol = o.grad_tol;

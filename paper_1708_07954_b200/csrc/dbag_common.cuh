@@ -44,6 +44,7 @@ struct DevState {
   double* ref_pts;    // [N][3] or null
   // options
   double rho_x, rho_y, eps_depth, huber_delta;
+  double w_x, w_y;  // sqrt(0.5 * rho): the residual row weights (admm_solver.cpp:183-184)
   double grad_tol, step_tol, armijo_c, backtrack;
   int32_t inner_max_iters, lbfgs_memory, max_line_search, loss;
   // reductions
