@@ -30,6 +30,9 @@ using namespace dbag;
 #ifndef DBAG_EFFORT_ORDER
 #define DBAG_EFFORT_ORDER 1  // Huber K1 in last-round effort order (launch_local)
 #endif
+#ifndef DBAG_FAST_V3
+#define DBAG_FAST_V3 1  // k_local_persistent3 (unified projection, CTA phase barrier)
+#endif
 #ifndef DBAG_FAST_PERSIST
 #define DBAG_FAST_PERSIST 1  // FAST GN: persistent lane-refill K1 (dbag_local.cuh)
 #endif
@@ -239,20 +242,24 @@ struct dbag_solver {
     }
     if (opts.loss == DBAG_LOSS_SQUARED_L2) {
 #if DBAG_FAST_PERSIST
+#if DBAG_FAST_V3
+      auto* kern = k_local_persistent3;
+      const size_t smem = kFast3Smem;
+#else
+      auto* kern = k_local_persistent2;
+      const size_t smem = kFastPersistSmem;
+#endif
       static int resident = 0;
       if (resident == 0) {
         int sms = 0, per_sm = 0;
-        CK(cudaFuncSetAttribute(k_local_persistent2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kFastPersistSmem));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_persistent2, 128,
-                                                         kFastPersistSmem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
         resident = sms * (per_sm > 0 ? per_sm : 1);
       }
       CK(cudaMemsetAsync(S.work, 0, sizeof(unsigned long long), stream));
       const int64_t g = (int64_t)grid_for(count, 128);
-      k_local_persistent2<<<(unsigned)(g < resident ? g : resident), 128, kFastPersistSmem,
-                            stream>>>(S, begin, count);
+      kern<<<(unsigned)(g < resident ? g : resident), 128, smem, stream>>>(S, begin, count);
 #else
       k_local<0><<<grid_for(count, 128), 128, 0, stream>>>(S, begin, count);
 #endif

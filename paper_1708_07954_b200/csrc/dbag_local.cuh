@@ -445,4 +445,218 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent2(DevStat
   flush_counters(S, cnt);
 }
 
+
+// FAST L2 K1, v3: the EXACT kernel's structure (dbag_exact.cu) with the FAST
+// arithmetic of k_local_persistent2: one projection per loop iteration shared
+// by a fresh observation's start point and the trial point, the Jacobian
+// after the accept, one CTA barrier per iteration (the warps share the loop
+// body's instruction-cache lines), a warp-local queue of claimed
+// observations, warp-aggregated counters, and the accepted point's trig
+// values and camera-frame point in the shared slice (slots 36..44).
+constexpr int kFast3Scr = 45;
+constexpr size_t kFast3Smem = sizeof(double) * (9 + kFast3Scr) * 128;
+
+__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent3(DevState S, int64_t begin,
+                                                                         int64_t count) {
+  extern __shared__ double fp_dyn[];
+  unsigned nj = 0, nt = 0, na = 0;
+  GnProblem P;
+  P.tgt = fp_dyn + threadIdx.x;
+  // A0 0..8 | A1 9..17 | rhs 18..26 | H_kk 27..35 | trig 36..41 | w 42..44
+  double* sc = fp_dyn + 9 * 128 + threadIdx.x;
+  P.wx = S.w_x;  // admm_solver.cpp:183-184
+  P.wy = S.w_y;
+  P.eps = S.eps_depth;
+  const double wx2 = P.wx * P.wx, wy2 = P.wy * P.wy;
+  const double iwx2 = 1.0 / wx2, iwy2 = 1.0 / wy2;  // D^-1 of the undamped trial
+  bool busy = false, need_jac = false, exhausted = false;
+  int64_t b = -1;
+  int it = 0, pos = 0;
+  double lambda = 0.0, obj = 0.0, e0 = 0.0, e1 = 0.0;
+  double v[9];
+  WarpQueue wq;
+  for (;;) {
+    const int64_t idx = refill_batched<64>(S, !busy, count, exhausted, wq);
+    const bool fresh = idx >= 0;
+    if (fresh) {
+      b = begin + idx;
+      const int32_t j = S.blk_cam[b];
+      const int32_t i = S.blk_pt[b];
+      pos = S.blk_pos[b];
+      const PointRec rec = S.prec[pos];
+      const double* yb = S.ybar + 8 * (int64_t)j;
+      const double4 xb = S.xbar[i];
+      double sd[6], yv[7];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        v[3 + k] = S.cam_soa[(int64_t)k * S.L + b];
+        sd[k] = S.cam_soa[(int64_t)(6 + k) * S.L + b];
+      }
+#pragma unroll
+      for (int k = 0; k < 7; ++k) yv[k] = yb[k];
+      v[0] = rec.x0;
+      v[1] = rec.x1;
+      v[2] = rec.x2;
+      P.tgt[0] = xb.x - rec.r0 / S.rho_x;
+      P.tgt[128] = xb.y - rec.r1 / S.rho_x;
+      P.tgt[256] = xb.z - rec.r2 / S.rho_x;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) P.tgt[(3 + k) * 128] = yv[k] - sd[k] / S.rho_y;
+      P.z0 = rec.u;
+      P.z1 = rec.v;
+      P.f = yv[6];
+      busy = true;
+    }
+    if (!__syncthreads_or(busy)) {
+      if (__syncthreads_and(exhausted)) break;
+      continue;
+    }
+    if (__ballot_sync(0xffffffffu, busy) == 0) continue;
+    bool done = false;
+    // ---- damped solve by Woodbury (see k_local_persistent2)
+    double vt[9], d2 = 0.0;
+    bool proj = fresh;
+    if (busy && !fresh) {
+      double iD[9], u[9];
+      double c00 = 1.0, c01 = 0.0, c11 = 1.0, a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const double A0k = sc[k * 128], A1k = sc[(9 + k) * 128];
+        const double wk2 = k < 3 ? wx2 : wy2;
+        iD[k] = lambda > 0.0 ? fast_rcp(wk2 + lambda * fmax(sc[(27 + k) * 128], 1e-12))
+                             : (k < 3 ? iwx2 : iwy2);
+        u[k] = sc[(18 + k) * 128] * iD[k];
+        c00 += A0k * A0k * iD[k];
+        c01 += A0k * A1k * iD[k];
+        c11 += A1k * A1k * iD[k];
+        a0 += A0k * u[k];
+        a1 += A1k * u[k];
+      }
+      const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
+      const double y0 = (c11 * a0 - c01 * a1) * idet;
+      const double y1 = (c00 * a1 - c01 * a0) * idet;
+      bool fin = true;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const double dk = u[k] - iD[k] * (sc[k * 128] * y0 + sc[(9 + k) * 128] * y1);
+        fin = fin && isfinite(dk);
+        d2 += dk * dk;
+        vt[k] = v[k] + dk;
+      }
+      proj = fin;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) vt[k] = v[k];
+    }
+    // ---- one projection + objective
+    bool accepted = false;
+    if (proj) {
+      Trig trt;
+      double Rt[9], wt[3], et0 = 0.0, et1 = 0.0, objt = 0.0;
+      const bool ok = gn_residual(P, vt, trt, Rt, wt, et0, et1, objt) && isfinite(et0) &&
+                      isfinite(et1) && isfinite(objt);
+      if (fresh || (ok && objt <= obj)) {  // start point / non-strict accept (:60)
+        if (ok) {
+          sc[36 * 128] = trt.sa;
+          sc[37 * 128] = trt.ca;
+          sc[38 * 128] = trt.sb;
+          sc[39 * 128] = trt.cb;
+          sc[40 * 128] = trt.sg;
+          sc[41 * 128] = trt.cg;
+          sc[42 * 128] = wt[0];
+          sc[43 * 128] = wt[1];
+          sc[44 * 128] = wt[2];
+          e0 = et0;
+          e1 = et1;
+          obj = objt;
+        }
+        if (fresh) {
+          if (ok) {
+            need_jac = true;
+            it = 0;
+          } else {  // the reference throws (local_opt.cpp:25-28)
+            atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)b);
+            busy = false;
+          }
+        } else {
+          accepted = true;
+          double x2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) {
+            v[k] = vt[k];
+            x2 += v[k] * v[k];
+          }
+          if (sqrt(d2) <= S.step_tol * (1.0 + sqrt(x2))) {
+            done = true;  // kStepConverged
+          } else {
+            ++it;
+            need_jac = true;
+          }
+        }
+      }
+    }
+    if (busy && !fresh && !accepted) {
+      lambda = lambda == 0.0 ? kDampingInit : lambda * 10.0;
+      if (lambda > kDampingMax) done = true;
+    }
+    nt += __popc(__ballot_sync(0xffffffffu, proj && !fresh));
+    na += __popc(__ballot_sync(0xffffffffu, accepted));
+    bool did_jac = false;
+    // ---- Jacobian and gradient at v
+    if (busy && need_jac && !done) {
+      if (it >= S.inner_max_iters) {
+        done = true;  // kMaxIters
+      } else {
+        Trig tr;
+        tr.sa = sc[36 * 128];
+        tr.ca = sc[37 * 128];
+        tr.sb = sc[38 * 128];
+        tr.cb = sc[39 * 128];
+        tr.sg = sc[40 * 128];
+        tr.cg = sc[41 * 128];
+        const double w[3] = {sc[42 * 128], sc[43 * 128], sc[44 * 128]};
+        double R[9], A0[9], A1[9];
+        rot_of(tr, R);
+        proj_jacobian(v, tr, R, w, P.f, A0, A1);
+        did_jac = true;
+        double g2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          const double wk = k < 3 ? P.wx : P.wy;
+          const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.T(k)));
+          sc[k * 128] = A0[k];
+          sc[(9 + k) * 128] = A1[k];
+          sc[(18 + k) * 128] = -jtr;  // rhs = -0.5 g
+          sc[(27 + k) * 128] = (A0[k] * A0[k] + A1[k] * A1[k]) + (k < 3 ? wx2 : wy2);
+          const double gk = 2.0 * jtr;  // g = 2 J^T r
+          g2 += gk * gk;
+        }
+        if (sqrt(g2) <= S.grad_tol) {
+          done = true;  // kGradConverged
+        } else {
+          need_jac = false;
+          lambda = 0.0;
+        }
+      }
+    }
+    nj += __popc(__ballot_sync(0xffffffffu, did_jac));
+    if (busy && done) {
+      double* xp = reinterpret_cast<double*>(S.prec + pos);
+      xp[0] = v[0];
+      xp[1] = v[1];
+      xp[2] = v[2];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) S.cam_soa[(int64_t)k * S.L + b] = v[3 + k];
+      busy = false;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long* slot =
+        S.counters + 8 * ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % kCounterStripes);
+    if (nj) atomicAdd(slot + 0, (unsigned long long)nj);
+    if (nt) atomicAdd(slot + 1, (unsigned long long)nt);
+    if (na) atomicAdd(slot + 2, (unsigned long long)na);
+  }
+}
+
 }  // namespace dbag

@@ -26,6 +26,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "fastv2": ["-DDBAG_FAST_V3=0"],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
     "pf0": ["-DDBAG_K1E_PREFETCH=0"],
     "pf0_sync0": ["-DDBAG_K1E_PREFETCH=0", "-DDBAG_K1E_SYNC=0"],
@@ -49,6 +50,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "fastv2": ["-DDBAG_FAST_V3=0"],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
     "pf0": ["-DDBAG_K1E_PREFETCH=0"],
     "pf0_sync0": ["-DDBAG_K1E_PREFETCH=0", "-DDBAG_K1E_SYNC=0"],
@@ -66,7 +68,9 @@ def main(names):
     saved = b.LIB
     for n in names or VARIANTS:
         b.LIB = os.path.join(out, n + ".so")
-        b.build(force=True, extra=VARIANTS[n], only=["dbag_exact.cu"])
+        fl = VARIANTS[n]
+        fast = any("DBAG_FAST" in f or "DBAG_K1_" in f for f in fl)
+        b.build(force=True, extra=fl, only=["dbag_capi.cu" if fast else "dbag_exact.cu"])
         print("built", b.LIB)
     b.LIB = saved
 
