@@ -134,9 +134,9 @@ __device__ __forceinline__ bool eproject(const double v[9], double f, double eps
 
 // try_project_with_jacobians (geometry.cpp:141-159) given cached t, R, w:
 // A0/A1 = [Jp | Jc] rows 0/1.
-__device__ __forceinline__ void ejac(const double v[9], const ETrig& t, const double R[9],
-                                     const double w[3], double f, double A0[9], double A1[9]) {
-  const double inv_z = __drcp_rn(w[2]);  // == 1.0 / w[2] (IEEE, round to nearest)
+__device__ __forceinline__ void ejac_inv(const double v[9], const ETrig& t, const double R[9],
+                                         const double w[3], double inv_z, double f, double A0[9],
+                                         double A1[9]) {
   const double d00 = f * inv_z, d02 = -f * w[0] * inv_z * inv_z;
   const double d11 = f * inv_z, d12 = -f * w[1] * inv_z * inv_z;
 #pragma unroll
@@ -158,6 +158,12 @@ __device__ __forceinline__ void ejac(const double v[9], const ETrig& t, const do
   A1[7] = d11;
   A0[8] = d02;
   A1[8] = d12;
+}
+
+// inv_z = __drcp_rn(w[2]) == 1.0 / w[2] (IEEE, round to nearest)
+__device__ __forceinline__ void ejac(const double v[9], const ETrig& t, const double R[9],
+                                     const double w[3], double f, double A0[9], double A1[9]) {
+  ejac_inv(v, t, R, w, __drcp_rn(w[2]), f, A0, A1);
 }
 
 __device__ __forceinline__ double sqn(const double* a, int n) {
