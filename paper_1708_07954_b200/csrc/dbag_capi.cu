@@ -236,8 +236,10 @@ struct dbag_solver {
       return;
     }
     if (exact()) {
-      CK(exact::launch_local(opts.loss == DBAG_LOSS_HUBER ? effort_order(begin, count) : S, begin,
-                             count, stream));
+      CK(exact::launch_local(opts.loss == DBAG_LOSS_HUBER && !exact::huber_persistent()
+                                 ? effort_order(begin, count)
+                                 : S,
+                             begin, count, stream));
       return;
     }
     if (opts.loss == DBAG_LOSS_SQUARED_L2) {

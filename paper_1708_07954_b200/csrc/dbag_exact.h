@@ -13,5 +13,7 @@ cudaError_t launch_local(const DevState& S, int64_t begin, int64_t count, cudaSt
 cudaError_t launch_camera(const DevState& S, int mode, cudaStream_t st);
 cudaError_t launch_point(const DevState& S, int mode, bool metric, int n_parts, cudaStream_t st);
 cudaError_t launch_camR_all(const DevState& S, cudaStream_t st);
+// the Huber K1 is the persistent lane-refill kernel (block order, no effort sort)
+bool huber_persistent();
 }  // namespace exact
 }  // namespace dbag

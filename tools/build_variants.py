@@ -26,6 +26,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "hubp0": ["-DDBAG_K1E_HUBP=0"],
     "fastv2": ["-DDBAG_FAST_V3=0"],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
     "pf0": ["-DDBAG_K1E_PREFETCH=0"],
@@ -50,6 +51,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "hubp0": ["-DDBAG_K1E_HUBP=0"],
     "fastv2": ["-DDBAG_FAST_V3=0"],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
     "pf0": ["-DDBAG_K1E_PREFETCH=0"],
