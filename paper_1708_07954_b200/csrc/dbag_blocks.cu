@@ -381,6 +381,18 @@ __device__ __forceinline__ void pivot_order(const Blk& k, const Carve& c) {
 // Result in c.dl. Scratch: c.dl / c.vt (temp[] double buffer), c.hdg is kept.
 __device__ __forceinline__ int rowp(int i) { return i * (i + 1) / 2; }
 
+#ifndef DBAG_GEN_COLMAJOR
+#define DBAG_GEN_COLMAJOR 0  // measured slower at (32,1): 43.3 vs 39.1 ms per round, config 2
+#endif
+#if DBAG_GEN_COLMAJOR
+// M packed by columns: column j holds rows j..D-1 contiguously, so a warp's
+// lanes (consecutive rows) read consecutive doubles (no bank conflicts).
+__device__ __forceinline__ int colp(int j, int D) { return j * D - j * (j - 1) / 2; }
+__device__ __forceinline__ int mix(int i, int j, int D) { return colp(j, D) + i - j; }
+#else
+__device__ __forceinline__ int mix(int i, int j, int D) { return rowp(i) + j; }
+#endif
+
 template <int kT, bool kSharedM>
 __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double* M) {
   const int D = k.D;
@@ -393,7 +405,7 @@ __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double*
     while (rowp(p) > e) --p;
     const int q = e - rowp(p);
     const int i = c.ord[p], j = c.ord[q];
-    M[e] = p == q ? c.hd[i] : h_entry(k, c, i, j);
+    M[mix(p, q, D)] = p == q ? c.hd[i] : h_entry(k, c, i, j);
   }
   for (int p = gtid<kT>(); p < D; p += kT) c.x[p] = c.g[c.ord[p]];  // P rhs (g holds rhs)
   gsync<kT>();
@@ -407,39 +419,46 @@ __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double*
     double* tn = tbuf[(kk + 1) & 1];
     if (kk > 0) {
       for (int i = kk + gtid<kT>(); i < D; i += kT) {
-        double* Mi = M + rowp(i);
         double s = 0.0;
+#if DBAG_GEN_COLMAJOR
+        int a = i;  // mix(i, 0)
+#pragma unroll 4
+        for (int j = 0; j < kk; ++j) {
+          s += M[a] * tc[j];
+          a += D - j - 1;  // mix(i, j + 1) - mix(i, j)
+        }
+#else
+        const double* Mi = M + rowp(i);
         for (int j = 0; j < kk; ++j) s += Mi[j] * tc[j];
-        Mi[kk] = Mi[kk] - s;
+#endif
+        M[mix(i, kk, D)] = M[mix(i, kk, D)] - s;
       }
       gsync<kT>();
     }
-    const double akk = M[rowp(kk) + kk];
+    const double akk = M[mix(kk, kk, D)];
     const bool valid = fabs(akk) > 0.0;
     if (kk == 0 && !valid) {
       stop = true;  // Eigen: all-zero diagonal, nothing factorized
     } else {
       for (int i = kk + 1 + gtid<kT>(); i < D; i += kT) {
-        double* Mi = M + rowp(i);
-        if (valid) Mi[kk] = Mi[kk] / akk;
-        if (i == kk + 1) tn[kk] = M[rowp(kk) + kk] * Mi[kk];  // D_kk L_{kk+1,kk}
+        const int e = mix(i, kk, D);
+        if (valid) M[e] = M[e] / akk;
+        if (i == kk + 1) tn[kk] = akk * M[e];  // D_kk L_{kk+1,kk}
       }
-      if (kk + 1 < D) {
-        const double* Mn = M + rowp(kk + 1);
-        for (int j = gtid<kT>(); j < kk; j += kT) tn[j] = M[rowp(j) + j] * Mn[j];
-      }
+      if (kk + 1 < D)
+        for (int j = gtid<kT>(); j < kk; j += kT) tn[j] = M[mix(j, j, D)] * M[mix(kk + 1, j, D)];
     }
     gsync<kT>();
   }
   // forward substitution, column sweep (same per-row order as the oracle)
   for (int j = 0; j < D - 1; ++j) {
     const double xj = c.x[j];
-    for (int i = j + 1 + gtid<kT>(); i < D; i += kT) c.x[i] = c.x[i] - M[rowp(i) + j] * xj;
+    for (int i = j + 1 + gtid<kT>(); i < D; i += kT) c.x[i] = c.x[i] - M[mix(i, j, D)] * xj;
     gsync<kT>();
   }
   const double tol = 2.2250738585072014e-308;  // DBL_MIN
   for (int i = gtid<kT>(); i < D; i += kT) {
-    const double d = M[rowp(i) + i];
+    const double d = M[mix(i, i, D)];
     c.x[i] = fabs(d) > tol ? c.x[i] / d : 0.0;
   }
   gsync<kT>();
@@ -447,8 +466,7 @@ __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double*
   // for j = D-1 down to 1)
   for (int j = D - 1; j > 0; --j) {
     const double xj = c.x[j];
-    const double* Mj = M + rowp(j);
-    for (int i = gtid<kT>(); i < j; i += kT) c.x[i] = c.x[i] - Mj[i] * xj;
+    for (int i = gtid<kT>(); i < j; i += kT) c.x[i] = c.x[i] - M[mix(j, i, D)] * xj;
     gsync<kT>();
   }
   for (int p = gtid<kT>(); p < D; p += kT) c.dl[c.ord[p]] = c.x[p];  // P^T y

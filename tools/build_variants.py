@@ -26,6 +26,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
     "hubp0": ["-DDBAG_K1E_HUBP=0"],
     "fastv2": ["-DDBAG_FAST_V3=0"],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
@@ -51,6 +52,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
     "hubp0": ["-DDBAG_K1E_HUBP=0"],
     "fastv2": ["-DDBAG_FAST_V3=0"],
     "batch0": ["-DDBAG_K1E_BATCH=0"],
@@ -72,7 +74,9 @@ def main(names):
         b.LIB = os.path.join(out, n + ".so")
         fl = VARIANTS[n]
         fast = any("DBAG_FAST" in f or "DBAG_K1_" in f for f in fl)
-        b.build(force=True, extra=fl, only=["dbag_capi.cu" if fast else "dbag_exact.cu"])
+        gen = any("DBAG_GEN" in f for f in fl)
+        b.build(force=True, extra=fl, only=["dbag_blocks.cu" if gen else
+                                            "dbag_capi.cu" if fast else "dbag_exact.cu"])
         print("built", b.LIB)
     b.LIB = saved
 
