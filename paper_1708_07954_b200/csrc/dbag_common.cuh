@@ -167,6 +167,56 @@ __device__ __forceinline__ int64_t refill_batched(const DevState& S, bool idle, 
   return idx < (unsigned long long)count ? (int64_t)idx : -1;
 }
 
+// refill_batched with the warp's queue in shared memory (warp-uniform state
+// off the register file): every lane reads it, the leader writes it back.
+struct WarpQueueS {
+  unsigned long long q0, q1;
+  unsigned end;
+};
+template <int kBatch>
+__device__ __forceinline__ int64_t refill_batched_s(const DevState& S, bool idle, int64_t count,
+                                                    bool& exhausted, WarpQueueS* q) {
+  const unsigned full = 0xffffffffu;
+  const unsigned m = __ballot_sync(full, idle && !exhausted);
+  if (m == 0) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  const unsigned n = __popc(m);
+  const unsigned rank = __popc(m & ((1u << lane) - 1u));
+  unsigned long long q0 = q->q0, q1 = q->q1;
+  bool end = q->end != 0;
+  const unsigned long long r = q1 - q0;
+  unsigned long long idx;
+  if (r >= n) {
+    idx = q0 + rank;
+    q0 += n;
+  } else {
+    const unsigned need = n - (unsigned)r;
+    const unsigned want = need > (unsigned)kBatch ? need : (unsigned)kBatch;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(S.work, (unsigned long long)want);
+    base = __shfl_sync(full, base, leader);
+    idx = rank < r ? q0 + rank : base + (rank - r);
+    q0 = base + need;
+    q1 = base + want;
+    if (q1 >= (unsigned long long)count) {
+      end = true;
+      q1 = (unsigned long long)count;
+      if (q0 > q1) q0 = q1;
+    }
+  }
+  __syncwarp();
+  if (lane == leader) {
+    q->q0 = q0;
+    q->q1 = q1;
+    q->end = end;
+  }
+  __syncwarp();
+  if (end && q0 >= q1) exhausted = true;
+  if (!(m & (1u << lane))) return -1;
+  return idx < (unsigned long long)count ? (int64_t)idx : -1;
+}
+
 // DevRecord layout (doubles)
 enum RecField {
   kRecSumErr = 0, kRecMaxPx, kRecMaxPy, kRecMaxDx, kRecMaxDy, kRecInfeasible, kRecCamMse,

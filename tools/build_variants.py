@@ -26,6 +26,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "lean0": ["-DDBAG_K1E_LEAN=0"],
     "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
     "hubp0": ["-DDBAG_K1E_HUBP=0"],
     "fastv2": ["-DDBAG_FAST_V3=0"],
@@ -52,6 +53,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "lean0": ["-DDBAG_K1E_LEAN=0"],
     "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
     "hubp0": ["-DDBAG_K1E_HUBP=0"],
     "fastv2": ["-DDBAG_FAST_V3=0"],
