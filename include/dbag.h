@@ -224,6 +224,10 @@ int dbag_reset_stats(dbag_solver* h);
 /* FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA): the FP64
  * roofline denominator, which MEASURED_PEAKS.json does not carry. */
 int dbag_measure_fp64_peak(int32_t device, double* tflops);
+/* Test hook (no reference counterpart): runs n of the EXACT kernels'
+ * branch-free reciprocals RN(1/d) over the exponent band they are used on and
+ * counts the results that differ bitwise from IEEE 1.0/d. */
+int dbag_selftest_division(int32_t device, int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* ---- multi-GPU ---------------------------------------------
  * Cameras are split into contiguous ranges balanced on observation counts;

@@ -142,6 +142,7 @@ SIGNATURES = {
     "dbag_get_round_stats": (C.c_int, [H, C.POINTER(RoundStats)]),
     "dbag_reset_stats": (C.c_int, [H]),
     "dbag_measure_fp64_peak": (C.c_int, [C.c_int32, DPTR]),
+    "dbag_selftest_division": (C.c_int, [C.c_int32, C.c_int64, C.c_uint64, I64P]),
     "dbag_partition_cameras": (C.c_int, [C.c_int32, I64P, C.c_int32, I32P]),
     "dbag_shard_plan_create": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int32,
                                          C.POINTER(H), C.POINTER(ShardInfo)]),

@@ -706,6 +706,14 @@ def measure_fp64_peak(device=0):
     return out.value
 
 
+def selftest_division(n, seed=1, device=0):
+    """Test hook: mismatches of the EXACT kernels' branch-free RN(1/d) against
+    IEEE 1.0/d over n operands of the guarded exponent band."""
+    out = C.c_int64()
+    _check(_capi.load().dbag_selftest_division(device, n, seed, C.byref(out)))
+    return out.value
+
+
 def run_admm(problem, init, opts=None, reference=None):
     """admm_solver.cpp:476-480 -> (final consensus, trace)."""
     solver = AdmmSolver(problem, init, opts)

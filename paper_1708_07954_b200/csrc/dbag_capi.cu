@@ -1464,6 +1464,20 @@ static __global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iter
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+int dbag_selftest_division(int32_t device, int64_t n, uint64_t seed, int64_t* mismatches) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(unsigned long long)));
+    CK(cudaMemset(d, 0, sizeof(unsigned long long)));
+    CK(exact::selftest_rcp(n, seed, d));
+    unsigned long long h = 0;
+    CK(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *mismatches = (int64_t)h;
+  });
+}
+
 int dbag_measure_fp64_peak(int32_t device, double* tflops) {
   return guarded([&] {
     CK(cudaSetDevice(device));

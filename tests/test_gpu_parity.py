@@ -493,3 +493,12 @@ def test_cpp_driver_file_mode_round_trip(O, P, tmp_path):
     opose, _, opts = osol.consensus()
     assert np.array_equal(solved.cam_pose, opose) and np.array_equal(solved.points, opts)
     assert csv.read_text().count("\n") == 16
+
+
+@pytest.mark.gpu
+def test_branch_free_reciprocal_is_ieee():
+    """The EXACT K1's branch-free RN(1/d) (dbag_exact.cu rcp_rn_fast: the fast
+    path nvcc emits for 1.0/d) equals IEEE 1.0/d bit for bit over its band."""
+    import paper_1708_07954_b200.admm as A
+    for seed in (1, 2, 3):
+        assert A.selftest_division(1 << 26, seed) == 0

@@ -26,6 +26,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "rcpfast0": ["-DDBAG_K1E_RCPFAST=0"],
     "lean0": ["-DDBAG_K1E_LEAN=0"],
     "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
     "hubp0": ["-DDBAG_K1E_HUBP=0"],
@@ -53,6 +54,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "rcpfast0": ["-DDBAG_K1E_RCPFAST=0"],
     "lean0": ["-DDBAG_K1E_LEAN=0"],
     "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
     "hubp0": ["-DDBAG_K1E_HUBP=0"],
