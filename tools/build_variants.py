@@ -26,6 +26,13 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "t96": ["-DDBAG_K1E_THREADS=96"],
+    "t64": ["-DDBAG_K1E_THREADS=64"],
+    "t160": ["-DDBAG_K1E_THREADS=160", "-DDBAG_K1E_MINB=2"],
+    "t192": ["-DDBAG_K1E_THREADS=192"],
+    "t384": ["-DDBAG_K1E_THREADS=384"],
+    "sync2": ["-DDBAG_K1E_SYNC=2"],
+    "sync4": ["-DDBAG_K1E_SYNC=4"],
     "rcpfast0": ["-DDBAG_K1E_RCPFAST=0"],
     "lean0": ["-DDBAG_K1E_LEAN=0"],
     "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
@@ -54,6 +61,13 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "t96": ["-DDBAG_K1E_THREADS=96"],
+    "t64": ["-DDBAG_K1E_THREADS=64"],
+    "t160": ["-DDBAG_K1E_THREADS=160", "-DDBAG_K1E_MINB=2"],
+    "t192": ["-DDBAG_K1E_THREADS=192"],
+    "t384": ["-DDBAG_K1E_THREADS=384"],
+    "sync2": ["-DDBAG_K1E_SYNC=2"],
+    "sync4": ["-DDBAG_K1E_SYNC=4"],
     "rcpfast0": ["-DDBAG_K1E_RCPFAST=0"],
     "lean0": ["-DDBAG_K1E_LEAN=0"],
     "colmajor0": ["-DDBAG_GEN_COLMAJOR=0"],
