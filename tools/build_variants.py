@@ -26,6 +26,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "split1": ["-DDBAG_K1E_SPLITREFILL=1"],
     "t96": ["-DDBAG_K1E_THREADS=96"],
     "t64": ["-DDBAG_K1E_THREADS=64"],
     "t160": ["-DDBAG_K1E_THREADS=160", "-DDBAG_K1E_MINB=2"],
@@ -61,6 +62,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "split1": ["-DDBAG_K1E_SPLITREFILL=1"],
     "t96": ["-DDBAG_K1E_THREADS=96"],
     "t64": ["-DDBAG_K1E_THREADS=64"],
     "t160": ["-DDBAG_K1E_THREADS=160", "-DDBAG_K1E_MINB=2"],
