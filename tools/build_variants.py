@@ -26,6 +26,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "fsync0": ["-DDBAG_K1_SYNC=0"],
     "split1": ["-DDBAG_K1E_SPLITREFILL=1"],
     "t96": ["-DDBAG_K1E_THREADS=96"],
     "t64": ["-DDBAG_K1E_THREADS=64"],
@@ -62,6 +63,7 @@ VARIANTS = {
     "mdiv0": ["-DDBAG_K1E_MDIV=0"],
     "mdiv1": ["-DDBAG_K1E_MDIV=1"],
     "cur": [],
+    "fsync0": ["-DDBAG_K1_SYNC=0"],
     "split1": ["-DDBAG_K1E_SPLITREFILL=1"],
     "t96": ["-DDBAG_K1E_THREADS=96"],
     "t64": ["-DDBAG_K1E_THREADS=64"],
