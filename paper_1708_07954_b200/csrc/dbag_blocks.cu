@@ -376,6 +376,49 @@ __device__ __forceinline__ void pivot_order(const Blk& k, const Carve& c) {
   }
 }
 
+#ifndef DBAG_GEN_PARPIV
+#define DBAG_GEN_PARPIV 1
+#endif
+// The same pivot order in parallel, verified: every thread ranks its
+// variables by |hd| (descending, ties by index) and scatters them. The
+// selection loop yields exactly that order when the sorted values are
+// strictly decreasing except for ties between consecutive variables (i, i+1)
+// sorted to positions p, p+1 with p <= i: variables i and i+1 keep positions
+// i and i+1 until step i (a variable moves only when displaced at its own
+// position), so when their value becomes the largest at step p <= i, i comes
+// first. This covers the structural ties, t_x and t_y of a camera (d00 ==
+// d11 in every observation's Jacobian). Anything else (other ties, NaN)
+// falls back to pivot_order. tests/test_pivot_network.py checks the rule.
+template <int kT>
+__device__ __forceinline__ void pivot_order_par(const Blk& k, const Carve& c) {
+  const int D = k.D;
+  if (gtid<kT>() == 0) c.flag[6] = 0;
+  gsync<kT>();
+  for (int i = gtid<kT>(); i < D; i += kT) {
+    const double ai = fabs(c.hd[i]);
+    int r = 0;
+    for (int j = 0; j < D; ++j) {
+      const double aj = fabs(c.hd[j]);
+      r += (aj > ai || (aj == ai && j < i)) ? 1 : 0;
+    }
+    if (!(ai == ai) || r >= D) c.flag[6] = 1;  // NaN: ranks are not a permutation
+    else c.ord[r] = i;
+  }
+  gsync<kT>();
+  if (c.flag[6] == 0) {
+    for (int p = gtid<kT>(); p + 1 < D; p += kT) {
+      const int a = c.ord[p], b = c.ord[p + 1];
+      const double x = fabs(c.hd[a]), y = fabs(c.hd[b]);
+      if (!(x > y || (x == y && b == a + 1 && p <= a))) c.flag[6] = 1;
+    }
+  }
+  gsync<kT>();
+  if (c.flag[6] != 0) {
+    gsync<kT>();
+    pivot_order<kT>(k, c);
+  }
+}
+
 // delta = (P^T LDL^T P)^{-1} rhs for Hd (oracle ldlt_solve on the permuted
 // system). M: lower triangle of P Hd P^T (row p at p(p+1)/2), filled here.
 // Result in c.dl. Scratch: c.dl / c.vt (temp[] double buffer), c.hdg is kept.
@@ -396,7 +439,11 @@ __device__ __forceinline__ int mix(int i, int j, int D) { return rowp(i) + j; }
 template <int kT, bool kSharedM>
 __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double* M) {
   const int D = k.D;
+#if DBAG_GEN_PARPIV
+  pivot_order_par<kT>(k, c);
+#else
   pivot_order<kT>(k, c);
+#endif
   gsync<kT>();
   const int ne = rowp(D);
   for (int e = gtid<kT>(); e < ne; e += kT) {

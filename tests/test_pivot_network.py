@@ -79,3 +79,54 @@ def test_shortcut_equals_selection_loop_when_accepted():
             accepted += 1
             assert f == selection_order(a), (a, f)
     assert accepted > 20000
+
+
+def selection_order_n(a):
+    a, o = list(a), list(range(len(a)))
+    n = len(a)
+    for k in range(n):
+        big, best = k, a[k]
+        for i in range(k + 1, n):
+            if a[i] > best:
+                best, big = a[i], i
+        a[k], a[big] = a[big], a[k]
+        o[k], o[big] = o[big], o[k]
+    return o
+
+
+def parallel_order(a):
+    """dbag_blocks.cu pivot_order_par: ranks (descending, ties by index) and the
+    acceptance rule; None = fall back to the selection loop."""
+    n = len(a)
+    if any(x != x for x in a):
+        return None
+    o = sorted(range(n), key=lambda i: (-a[i], i))
+    for p in range(n - 1):
+        x, y, i, j = a[o[p]], a[o[p + 1]], o[p], o[p + 1]
+        if not (x > y or (x == y and j == i + 1 and p <= i)):
+            return None
+    return o
+
+
+def test_generalized_parallel_pivot_rule():
+    """Blocks of D variables with the camera t_x/t_y ties (consecutive indices)."""
+    rng = np.random.default_rng(1)
+    accepted = 0
+    for t in range(4000):
+        npt, ncam = int(rng.integers(1, 12)), int(rng.integers(1, 4))
+        D = 3 * npt + 6 * ncam
+        a = list(rng.uniform(0.5, 2.0, D) * 10.0 ** rng.uniform(-1, 4, D))
+        cams = 10.0 ** rng.uniform(0, 6)
+        for c in range(ncam):   # cameras: often the largest values, t_x == t_y
+            base = 3 * npt + 6 * c
+            for m in range(6):
+                a[base + m] = cams * rng.uniform(0.1, 10.0)
+            a[base + 4] = a[base + 3]
+        if t % 5 == 0:          # an accidental tie elsewhere: must fall back or agree
+            i, j = rng.integers(0, D, 2)
+            a[i] = a[j]
+        f = parallel_order(a)
+        if f is not None:
+            accepted += 1
+            assert f == selection_order_n(a), (a, f)
+    assert accepted > 1000

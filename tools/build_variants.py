@@ -33,6 +33,7 @@ VARIANTS = {
     "fast_minb3": ["-DDBAG_K1_MINB=3"],
     # generalized blocks (dbag_blocks.cu)
     "gen_colmajor": ["-DDBAG_GEN_COLMAJOR=1"],
+    "gen_parpiv0": ["-DDBAG_GEN_PARPIV=0"],
 }
 
 
