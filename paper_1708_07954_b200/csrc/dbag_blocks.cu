@@ -447,7 +447,7 @@ __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double*
   gsync<kT>();
   const int ne = rowp(D);
   for (int e = gtid<kT>(); e < ne; e += kT) {
-    int p = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+    int p = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);  // approximate; fixed below
     while (rowp(p + 1) <= e) ++p;
     while (rowp(p) > e) --p;
     const int q = e - rowp(p);

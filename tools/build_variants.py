@@ -34,6 +34,8 @@ VARIANTS = {
     # generalized blocks (dbag_blocks.cu)
     "gen_colmajor": ["-DDBAG_GEN_COLMAJOR=1"],
     "gen_parpiv0": ["-DDBAG_GEN_PARPIV=0"],
+    "gen_warp128": ["-DDBAG_WARP_BLOCK_MAX_DIM=128", "-DDBAG_GEN_X"],
+    "gen_warp24": ["-DDBAG_WARP_BLOCK_MAX_DIM=24", "-DDBAG_GEN_X"],
 }
 
 
