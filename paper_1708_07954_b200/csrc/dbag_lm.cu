@@ -23,6 +23,8 @@
 // (use_schur = 0), limited to small systems.
 #include <cusolverDn.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -738,6 +740,59 @@ struct dbag_lm {
 
 extern "C" {
 
+// ---- Schur pair lists on the device ------------------------------------------
+// Every point contributes one triplet (obs a, obs b, point) per ordered pair of
+// its observations to the list of block (cam a, cam b). Emitted point-major
+// (points ascending, then a, then b: the host loop's order), then a stable
+// radix sort by block key keeps that order inside each block's list.
+__global__ void k_pair_count(int n, const int64_t* po, int64_t* cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int64_t d = po[i + 1] - po[i];
+    cnt[i] = d * d;
+  }
+}
+
+__global__ void k_pair_emit(int n, int m, const int64_t* po, const int32_t* pobs,
+                            const int32_t* cam, const int64_t* toff, uint32_t* key,
+                            int32_t* ta, int32_t* tb, int32_t* ti, int32_t* idx) {
+  // a warp per point: lanes stride over its d*d ordered pairs
+  const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t b0 = po[i], d = po[i + 1] - po[i], t0 = toff[i];
+  for (int64_t e = lane; e < d * d; e += 32) {
+    const int32_t ka = pobs[b0 + e / d], kb = pobs[b0 + e % d];
+    const int64_t t = t0 + e;
+    key[t] = (uint32_t)cam[ka] * (uint32_t)m + (uint32_t)cam[kb];
+    ta[t] = ka;
+    tb[t] = kb;
+    ti[t] = i;
+    idx[t] = (int32_t)t;
+  }
+}
+
+__global__ void k_pair_gather(int64_t T, const int32_t* perm, const int32_t* ta,
+                              const int32_t* tb, const int32_t* ti, int32_t* oa, int32_t* ob,
+                              int32_t* oi) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = perm[t];
+    oa[t] = ta[s];
+    ob[t] = tb[s];
+    oi[t] = ti[s];
+  }
+}
+
+__global__ void k_pair_blocks(int64_t npairs, int m, const uint32_t* ukey, int32_t* ja,
+                              int32_t* jb) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    ja[p] = (int32_t)(ukey[p] / (uint32_t)m);
+    jb[p] = (int32_t)(ukey[p] % (uint32_t)m);
+  }
+}
+
 void dbag_lm_options_default(dbag_lm_options* o) {  // lm_solver.hpp:14-23
   o->max_iters = 100;
   o->error_stop = 1e-14;
@@ -802,66 +857,9 @@ int dbag_lm_create(const dbag_problem_view* p, const dbag_param_view* init,
           cobs_p[fcp[p->obs_cam[k]]++] = k;
         }
     }
-    // Schur pair lists: for every point (ascending) and every ordered pair of
-    // its observations, a triplet in the list of block (cam a, cam b)
-    std::vector<int64_t> pair_id((size_t)m * m, 0);
-    for (int i = 0; i < n; ++i)
-      for (int64_t qa = po[i]; qa < po[i + 1]; ++qa)
-        for (int64_t qb = po[i]; qb < po[i + 1]; ++qb)
-          ++pair_id[(size_t)p->obs_cam[pobs[qa]] * m + p->obs_cam[pobs[qb]]];
-    std::vector<int32_t> pja, pjb;
-    std::vector<int64_t> poff(1, 0);
-    for (int ja = 0; ja < m; ++ja)
-      for (int jb = 0; jb < m; ++jb) {
-        int64_t& c = pair_id[(size_t)ja * m + jb];
-        if (c == 0) {
-          c = -1;
-          continue;
-        }
-        pja.push_back(ja);
-        pjb.push_back(jb);
-        poff.push_back(poff.back() + c);
-        c = (int64_t)pja.size() - 1;
-      }
-    std::vector<int32_t> ta(poff.back()), tb(poff.back()), ti(poff.back());
-    {
-      std::vector<int64_t> fill(poff.begin(), poff.end() - 1);
-      for (int i = 0; i < n; ++i)
-        for (int64_t qa = po[i]; qa < po[i + 1]; ++qa)
-          for (int64_t qb = po[i]; qb < po[i + 1]; ++qb) {
-            const int32_t ka = pobs[qa], kb = pobs[qb];
-            const int64_t id = pair_id[(size_t)p->obs_cam[ka] * m + p->obs_cam[kb]];
-            const int64_t pos = fill[id]++;
-            ta[pos] = ka;
-            tb[pos] = kb;
-            ti[pos] = i;
-          }
-    }
     auto up = [&](auto* dst, const void* src, size_t bytes) {
       LK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->st));
     };
-    {
-      int32_t* dja = h->alloc<int32_t>(pja.size());
-      int32_t* djb = h->alloc<int32_t>(pjb.size());
-      int64_t* dpo = h->alloc<int64_t>(poff.size());
-      int32_t* dta = h->alloc<int32_t>(ta.size());
-      int32_t* dtb = h->alloc<int32_t>(tb.size());
-      int32_t* dti = h->alloc<int32_t>(ti.size());
-      up(dja, pja.data(), 4 * pja.size());
-      up(djb, pjb.data(), 4 * pjb.size());
-      up(dpo, poff.data(), 8 * poff.size());
-      up(dta, ta.data(), 4 * ta.size());
-      up(dtb, tb.data(), 4 * tb.size());
-      up(dti, ti.data(), 4 * ti.size());
-      h->sync();  // the host vectors die at the end of this scope
-      d.npairs = (int64_t)pja.size();
-      d.pair_ja = dja;
-      d.pair_jb = djb;
-      d.pair_off = dpo;
-      d.trip_a = dta;
-      d.trip_b = dtb;
-      d.trip_i = dti;
-    }
     int32_t* dcam = h->alloc<int32_t>(l);
     int32_t* dpt = h->alloc<int32_t>(l);
     double* duv = h->alloc<double>(2 * l);
@@ -886,6 +884,87 @@ int dbag_lm_create(const dbag_problem_view* p, const dbag_param_view* init,
     d.cam_obs = dcobs;
     d.cam_obs_p = dcobs_p;
     d.pt_obs = dpobs;
+    {
+      // Schur pair lists on the device (k_pair_*): count d_i^2 triplets per
+      // point, emit them point-major, stable radix sort by block key, run
+      // lengths -> (ja, jb, offsets). Same lists, same order as the host loop
+      // over points / observation pairs it replaces.
+      auto tmp = [&](size_t bytes) {
+        void* q = nullptr;
+        LK(cudaMalloc(&q, bytes ? bytes : 1));
+        return q;
+      };
+      int64_t* cnt = static_cast<int64_t*>(tmp(8 * (size_t)(n + 1)));
+      int64_t* toff = static_cast<int64_t*>(tmp(8 * (size_t)(n + 1)));
+      k_pair_count<<<(n + 255) / 256, 256, 0, h->st>>>(n, dpo, cnt);
+      LK(cudaMemsetAsync(cnt + n, 0, 8, h->st));
+      size_t tb_bytes = 0;
+      LK(cub::DeviceScan::ExclusiveSum(nullptr, tb_bytes, cnt, toff, n + 1, h->st));
+      void* scan_tmp = tmp(tb_bytes);
+      LK(cub::DeviceScan::ExclusiveSum(scan_tmp, tb_bytes, cnt, toff, n + 1, h->st));
+      int64_t T = 0;
+      LK(cudaMemcpyAsync(&T, toff + n, 8, cudaMemcpyDeviceToHost, h->st));
+      h->sync();
+      if (T >= (int64_t)std::numeric_limits<int32_t>::max())
+        throw LmErr{DBAG_ERR_UNSUPPORTED, "more than 2^31 Schur triplets"};
+      uint32_t* key = static_cast<uint32_t*>(tmp(4 * (size_t)T));
+      uint32_t* key_s = static_cast<uint32_t*>(tmp(4 * (size_t)T));
+      int32_t* ta = static_cast<int32_t*>(tmp(4 * (size_t)T));
+      int32_t* tb = static_cast<int32_t*>(tmp(4 * (size_t)T));
+      int32_t* ti = static_cast<int32_t*>(tmp(4 * (size_t)T));
+      int32_t* idx = static_cast<int32_t*>(tmp(4 * (size_t)T));
+      int32_t* perm = static_cast<int32_t*>(tmp(4 * (size_t)T));
+      k_pair_emit<<<(unsigned)(((int64_t)n * 32 + 255) / 256), 256, 0, h->st>>>(
+          n, m, dpo, dpobs, dcam, toff, key, ta, tb, ti, idx);
+      LK(cudaGetLastError());
+      int bits = 1;
+      while (bits < 32 && ((uint64_t)m * (uint64_t)m >> bits) != 0) ++bits;
+      size_t sb = 0;
+      LK(cub::DeviceRadixSort::SortPairs(nullptr, sb, key, key_s, idx, perm, (int)T, 0, bits,
+                                         h->st));
+      void* sort_tmp = tmp(sb);
+      LK(cub::DeviceRadixSort::SortPairs(sort_tmp, sb, key, key_s, idx, perm, (int)T, 0, bits,
+                                         h->st));
+      int32_t* dta = h->alloc<int32_t>(T);
+      int32_t* dtb = h->alloc<int32_t>(T);
+      int32_t* dti = h->alloc<int32_t>(T);
+      k_pair_gather<<<592, 256, 0, h->st>>>(T, perm, ta, tb, ti, dta, dtb, dti);
+      LK(cudaGetLastError());
+      // run-length encode the sorted keys -> blocks and their triplet counts
+      uint32_t* ukey = key;  // reuse: the unsorted keys are dead
+      const int64_t max_runs = std::min<int64_t>(T, (int64_t)m * m);
+      int64_t* rc = static_cast<int64_t*>(tmp(8 * (size_t)(max_runs + 1)));
+      int64_t* nruns = static_cast<int64_t*>(tmp(8));
+      size_t rb = 0;
+      LK(cub::DeviceRunLengthEncode::Encode(nullptr, rb, key_s, ukey, rc, nruns, T, h->st));
+      void* rle_tmp = tmp(rb);
+      LK(cub::DeviceRunLengthEncode::Encode(rle_tmp, rb, key_s, ukey, rc, nruns, T, h->st));
+      int64_t npairs = 0;
+      LK(cudaMemcpyAsync(&npairs, nruns, 8, cudaMemcpyDeviceToHost, h->st));
+      h->sync();
+      int32_t* dja = h->alloc<int32_t>(npairs);
+      int32_t* djb = h->alloc<int32_t>(npairs);
+      int64_t* dpoff = h->alloc<int64_t>(npairs + 1);
+      LK(cudaMemsetAsync(rc + npairs, 0, 8, h->st));
+      size_t eb = 0;
+      LK(cub::DeviceScan::ExclusiveSum(nullptr, eb, rc, dpoff, npairs + 1, h->st));
+      void* ex_tmp = tmp(eb);
+      LK(cub::DeviceScan::ExclusiveSum(ex_tmp, eb, rc, dpoff, npairs + 1, h->st));
+      k_pair_blocks<<<592, 256, 0, h->st>>>(npairs, m, ukey, dja, djb);
+      LK(cudaGetLastError());
+      h->sync();
+      for (void* q : {(void*)cnt, (void*)toff, scan_tmp, (void*)key, (void*)key_s, (void*)ta,
+                      (void*)tb, (void*)ti, (void*)idx, (void*)perm, sort_tmp, (void*)rc,
+                      (void*)nruns, rle_tmp, ex_tmp})
+        cudaFree(q);
+      d.npairs = npairs;
+      d.pair_ja = dja;
+      d.pair_jb = djb;
+      d.pair_off = dpoff;
+      d.trip_a = dta;
+      d.trip_b = dtb;
+      d.trip_i = dti;
+    }
     d.J = h->alloc<double>(18 * l);
     d.r = h->alloc<double>(2 * l);
     d.W = h->alloc<double>(18 * l);
