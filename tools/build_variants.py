@@ -28,6 +28,7 @@ VARIANTS = {
     "exact_rcpfast0": ["-DDBAG_K1E_RCPFAST=0"],
     "exact_jacinline0": ["-DDBAG_K1E_JACINLINE=0"],
     "exact_lean2_0": ["-DDBAG_K1E_LEAN2=0"],
+    "exact_lean3_0": ["-DDBAG_K1E_LEAN3=0"],
     "exact_hubp": ["-DDBAG_K1E_HUBP=1"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
     "fast_v2": ["-DDBAG_FAST_V3=0"],
