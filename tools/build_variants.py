@@ -14,6 +14,7 @@ VARIANTS = {
     "cur": [],
     # EXACT K1 (dbag_exact.cu)
     "exact_t96": ["-DDBAG_K1E_THREADS=96"],
+    "exact_t64": ["-DDBAG_K1E_THREADS=64"],
     "exact_t128": ["-DDBAG_K1E_THREADS=128"],
     "exact_t384": ["-DDBAG_K1E_THREADS=384"],
     "exact_nosync": ["-DDBAG_K1E_SYNC=0"],
