@@ -30,6 +30,9 @@ using namespace dbag;
 #ifndef DBAG_EFFORT_ORDER
 #define DBAG_EFFORT_ORDER 1  // Huber K1 in last-round effort order (launch_local)
 #endif
+#ifndef DBAG_FAST_V4
+#define DBAG_FAST_V4 1  // k_local_persistent4 (Jacobian after accept, state in shared memory)
+#endif
 #ifndef DBAG_FAST_V3
 #define DBAG_FAST_V3 1  // k_local_persistent3 (unified projection, CTA phase barrier)
 #endif
@@ -244,7 +247,10 @@ struct dbag_solver {
     }
     if (opts.loss == DBAG_LOSS_SQUARED_L2) {
 #if DBAG_FAST_PERSIST
-#if DBAG_FAST_V3
+#if DBAG_FAST_V4
+      auto* kern = k_local_persistent4;
+      const size_t smem = kFast4Smem;
+#elif DBAG_FAST_V3
       auto* kern = k_local_persistent3;
       const size_t smem = kFast3Smem;
 #else

@@ -669,4 +669,226 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent3(DevStat
   }
 }
 
+
+// FAST L2 K1, v4: v3 with the EXACT kernel's later lessons: the Jacobian right
+// after an accept / start point from the residual's trig values, R and w in
+// registers (no accepted-state slots), the warp's index queue and counters in
+// shared memory, and lambda, the objective, the observation and the camera
+// pose copy in the shared slice instead of registers.
+constexpr int kFast4Scr = 46;  // A0 | A1 | rhs | H_kk (0..35), pose 36..41, lambda, obj, z0, z1
+constexpr size_t kFast4Smem = sizeof(double) * (9 + kFast4Scr) * 128;
+
+__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent4(DevState S, int64_t begin,
+                                                                         int64_t count) {
+  extern __shared__ double fp_dyn[];
+  __shared__ unsigned long long wcnt[4][3];
+  __shared__ WarpQueueS wqs[4];
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    wcnt[wid][0] = wcnt[wid][1] = wcnt[wid][2] = 0;
+    wqs[wid].q0 = wqs[wid].q1 = 0;
+    wqs[wid].end = 0;
+  }
+  __syncwarp();
+  GnProblem P;
+  P.tgt = fp_dyn + threadIdx.x;
+  double* sc = fp_dyn + 9 * 128 + threadIdx.x;
+#define VC(k) sc[(36 + (k)) * 128]
+#define LAM sc[42 * 128]
+#define OBJ sc[43 * 128]
+#define Z0 sc[44 * 128]
+#define Z1 sc[45 * 128]
+#define CNT(slot, pred)                                                \
+  {                                                                    \
+    const unsigned c_ = __popc(__ballot_sync(0xffffffffu, pred));      \
+    if ((threadIdx.x & 31) == 0 && c_) wcnt[wid][slot] += c_;         \
+  }
+  P.wx = S.w_x;  // admm_solver.cpp:183-184
+  P.wy = S.w_y;
+  P.eps = S.eps_depth;
+  const double wx2 = P.wx * P.wx, wy2 = P.wy * P.wy;
+  const double iwx2 = 1.0 / wx2, iwy2 = 1.0 / wy2;  // D^-1 of the undamped trial
+  bool busy = false, exhausted = false;
+  int64_t b = -1;
+  int it = 0, pos = 0;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;  // the point copy; the pose copy is VC
+  for (;;) {
+    const int64_t idx = refill_batched_s<64>(S, !busy, count, exhausted, &wqs[wid]);
+    const bool fresh = idx >= 0;
+    if (fresh) {
+      b = begin + idx;
+      const int32_t j = S.blk_cam[b];
+      const int32_t i = S.blk_pt[b];
+      pos = S.blk_pos[b];
+      const PointRec rec = S.prec[pos];
+      const double* yb = S.ybar + 8 * (int64_t)j;
+      const double4 xb = S.xbar[i];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        VC(k) = S.cam_soa[(int64_t)k * S.L + b];
+        P.tgt[(3 + k) * 128] = yb[k] - S.cam_soa[(int64_t)(6 + k) * S.L + b] / S.rho_y;
+      }
+      v0 = rec.x0;
+      v1 = rec.x1;
+      v2 = rec.x2;
+      P.tgt[0] = xb.x - rec.r0 / S.rho_x;
+      P.tgt[128] = xb.y - rec.r1 / S.rho_x;
+      P.tgt[256] = xb.z - rec.r2 / S.rho_x;
+      Z0 = rec.u;
+      Z1 = rec.v;
+      P.f = yb[6];
+      busy = true;
+    }
+#if DBAG_K1_SYNC
+    if (!__syncthreads_or(busy)) {
+      if (__syncthreads_and(exhausted)) break;
+      continue;
+    }
+    if (__ballot_sync(0xffffffffu, busy) == 0) continue;
+#else
+    if (__ballot_sync(0xffffffffu, busy) == 0) {
+      if (exhausted) break;
+      continue;
+    }
+#endif
+    bool done = false;
+    // ---- damped solve by Woodbury (see k_local_persistent2)
+    double vt[9], d2 = 0.0;
+    bool proj = fresh;
+    if (busy && !fresh) {
+      const double lambda = LAM;
+      double iD[9], u[9];
+      double c00 = 1.0, c01 = 0.0, c11 = 1.0, a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const double A0k = sc[k * 128], A1k = sc[(9 + k) * 128];
+        const double wk2 = k < 3 ? wx2 : wy2;
+        iD[k] = lambda > 0.0 ? fast_rcp(wk2 + lambda * fmax(sc[(27 + k) * 128], 1e-12))
+                             : (k < 3 ? iwx2 : iwy2);
+        u[k] = sc[(18 + k) * 128] * iD[k];
+        c00 += A0k * A0k * iD[k];
+        c01 += A0k * A1k * iD[k];
+        c11 += A1k * A1k * iD[k];
+        a0 += A0k * u[k];
+        a1 += A1k * u[k];
+      }
+      const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
+      const double y0 = (c11 * a0 - c01 * a1) * idet;
+      const double y1 = (c00 * a1 - c01 * a0) * idet;
+      bool fin = true;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const double dk = u[k] - iD[k] * (sc[k * 128] * y0 + sc[(9 + k) * 128] * y1);
+        fin = fin && isfinite(dk);
+        d2 += dk * dk;
+        vt[k] = (k == 0 ? v0 : k == 1 ? v1 : k == 2 ? v2 : VC(k - 3)) + dk;
+      }
+      proj = fin;
+    } else {
+      vt[0] = v0;
+      vt[1] = v1;
+      vt[2] = v2;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) vt[3 + k] = VC(k);
+    }
+    // ---- one projection + objective, then the Jacobian of a taken point
+    bool accepted = false, did_jac = false;
+    if (proj) {
+      Trig trt;
+      double Rt[9], wt[3], et0 = 0.0, et1 = 0.0, objt = 0.0;
+      P.z0 = Z0;
+      P.z1 = Z1;
+      const bool ok = gn_residual(P, vt, trt, Rt, wt, et0, et1, objt) && isfinite(et0) &&
+                      isfinite(et1) && isfinite(objt);
+      bool take = false;
+      if (fresh) {
+        if (ok) {
+          take = true;
+          it = 0;
+        } else {  // the reference throws (local_opt.cpp:25-28)
+          atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)b);
+          busy = false;
+        }
+      } else if (ok && objt <= OBJ) {  // non-strict accept (:60)
+        take = true;
+        accepted = true;
+        v0 = vt[0];
+        v1 = vt[1];
+        v2 = vt[2];
+        double x2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          if (k >= 3) VC(k - 3) = vt[k];
+          x2 += vt[k] * vt[k];
+        }
+        if (sqrt(d2) <= S.step_tol * (1.0 + sqrt(x2))) {
+          done = true;  // kStepConverged
+        } else {
+          ++it;
+        }
+      }
+      if (take) {
+        OBJ = objt;
+        if (!done) {
+          if (it >= S.inner_max_iters) {
+            done = true;  // kMaxIters
+          } else {
+            double A0[9], A1[9];
+            proj_jacobian(vt, trt, Rt, wt, P.f, A0, A1);
+            did_jac = true;
+            double g2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+              const double wk = k < 3 ? P.wx : P.wy;
+              const double jtr = -(A0[k] * et0 + A1[k] * et1) + wk * (wk * (vt[k] - P.T(k)));
+              sc[k * 128] = A0[k];
+              sc[(9 + k) * 128] = A1[k];
+              sc[(18 + k) * 128] = -jtr;  // rhs = -0.5 g
+              sc[(27 + k) * 128] = (A0[k] * A0[k] + A1[k] * A1[k]) + (k < 3 ? wx2 : wy2);
+              const double gk = 2.0 * jtr;  // g = 2 J^T r
+              g2 += gk * gk;
+            }
+            if (sqrt(g2) <= S.grad_tol) {
+              done = true;  // kGradConverged
+            } else {
+              LAM = 0.0;
+            }
+          }
+        }
+      }
+    }
+    if (busy && !fresh && !accepted) {
+      const double lam = LAM;
+      const double ln = lam == 0.0 ? kDampingInit : lam * 10.0;
+      LAM = ln;
+      if (ln > kDampingMax) done = true;
+    }
+    CNT(1, proj && !fresh);
+    CNT(2, accepted);
+    CNT(0, did_jac);
+    if (busy && done) {
+      double* xp = reinterpret_cast<double*>(S.prec + pos);
+      xp[0] = v0;
+      xp[1] = v1;
+      xp[2] = v2;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) S.cam_soa[(int64_t)k * S.L + b] = VC(k);
+      busy = false;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long* slot =
+        S.counters + 8 * ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % kCounterStripes);
+    if (wcnt[wid][0]) atomicAdd(slot + 0, wcnt[wid][0]);
+    if (wcnt[wid][1]) atomicAdd(slot + 1, wcnt[wid][1]);
+    if (wcnt[wid][2]) atomicAdd(slot + 2, wcnt[wid][2]);
+  }
+#undef VC
+#undef LAM
+#undef OBJ
+#undef Z0
+#undef Z1
+#undef CNT
+}
+
 }  // namespace dbag

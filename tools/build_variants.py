@@ -32,7 +32,8 @@ VARIANTS = {
     "exact_lean3_0": ["-DDBAG_K1E_LEAN3=0"],
     "exact_hubp": ["-DDBAG_K1E_HUBP=1"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
-    "fast_v2": ["-DDBAG_FAST_V3=0"],
+    "fast_v2": ["-DDBAG_FAST_V4=0", "-DDBAG_FAST_V3=0"],
+    "fast_v3": ["-DDBAG_FAST_V4=0"],
     "fast_sync": ["-DDBAG_K1_SYNC=1"],
     "fast_minb3": ["-DDBAG_K1_MINB=3"],
     # generalized blocks (dbag_blocks.cu)
