@@ -31,6 +31,8 @@ VARIANTS = {
     "exact_lean2_0": ["-DDBAG_K1E_LEAN2=0"],
     "exact_lean3_0": ["-DDBAG_K1E_LEAN3=0"],
     "exact_hubp": ["-DDBAG_K1E_HUBP=1"],
+    "exact_hub_minb2": ["-DDBAG_K1E_HUB_MINB=2"],
+    "exact_hub_minb4": ["-DDBAG_K1E_HUB_MINB=4"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
     "fast_v2": ["-DDBAG_FAST_V4=0", "-DDBAG_FAST_V3=0"],
     "fast_v3": ["-DDBAG_FAST_V4=0"],
