@@ -207,7 +207,10 @@ __device__ __noinline__ bool local_lbfgs(const DevState& S, const HuberProblem& 
   return true;  // kMaxIters
 }
 
-__global__ void __launch_bounds__(kHuberThreads) k_local_huber(DevState S, int64_t begin,
+#ifndef DBAG_K1_HUB_MINB
+#define DBAG_K1_HUB_MINB 1
+#endif
+__global__ void __launch_bounds__(kHuberThreads, DBAG_K1_HUB_MINB) k_local_huber(DevState S, int64_t begin,
                                                                int64_t count) {
   const int64_t tix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   LocalCounters cnt;

@@ -38,6 +38,8 @@ VARIANTS = {
     "fast_v3": ["-DDBAG_FAST_V4=0"],
     "fast_sync": ["-DDBAG_K1_SYNC=1"],
     "fast_minb3": ["-DDBAG_K1_MINB=3"],
+    "fast_hub_minb2": ["-DDBAG_K1_HUB_MINB=2"],
+    "fast_hub_minb3": ["-DDBAG_K1_HUB_MINB=3"],
     # generalized blocks (dbag_blocks.cu)
     "gen_colmajor": ["-DDBAG_GEN_COLMAJOR=1"],
     "gen_parpiv0": ["-DDBAG_GEN_PARPIV=0"],
