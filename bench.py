@@ -385,7 +385,7 @@ def our_arm(args, rank, world, local_rank):
     # local solves), from the committed profile of this numerics mode
     pipe = None
     prof = {"exact": "r1_k1_exact_markstein_config5s01.txt",
-            "fast": "r1_k1_fast_v3_config5s01.txt"}.get(args.numerics)
+            "fast": "r1_k1_fast_v4_config5s01.txt"}.get(args.numerics)
     if prof and not general and args.loss == "l2":
         try:
             for ln in open(os.path.join(ROOT, "profiles", prof)):

@@ -33,6 +33,10 @@ VARIANTS = {
     "exact_lean3_0": ["-DDBAG_K1E_LEAN3=0"],
     "exact_hubp": ["-DDBAG_K1E_HUBP=1"],
     "exact_hub_minb2": ["-DDBAG_K1E_HUB_MINB=2"],
+    "k2_group0": ["-DDBAG_K2E_GROUP=0"],
+    "k2_g4": ["-DDBAG_K2E_G=4"],
+    "k2_g2": ["-DDBAG_K2E_G=2"],
+    "k2_g16": ["-DDBAG_K2E_G=16"],
     "exact_hub_minb4": ["-DDBAG_K1E_HUB_MINB=4"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
     "fast_v2": ["-DDBAG_FAST_V4=0", "-DDBAG_FAST_V3=0"],
