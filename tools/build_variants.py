@@ -19,6 +19,8 @@ VARIANTS = {
     "exact_t384": ["-DDBAG_K1E_THREADS=384"],
     "exact_nosync": ["-DDBAG_K1E_SYNC=0"],
     "exact_sync2": ["-DDBAG_K1E_SYNC=2"],
+    "exact_syncg2": ["-DDBAG_K1E_SYNCGROUP=2"],
+    "exact_syncg2_t256": ["-DDBAG_K1E_SYNCGROUP=2", "-DDBAG_K1E_THREADS=256"],
     "exact_batch0": ["-DDBAG_K1E_BATCH=0", "-DDBAG_K1E_LEAN=0"],
     "exact_lean0": ["-DDBAG_K1E_LEAN=0"],
     "exact_prefetch": ["-DDBAG_K1E_PREFETCH=1", "-DDBAG_K1E_LEAN=0"],
