@@ -22,6 +22,8 @@ VARIANTS = {
     "exact_syncg2": ["-DDBAG_K1E_SYNCGROUP=2"],
     "exact_syncg2_t256": ["-DDBAG_K1E_SYNCGROUP=2", "-DDBAG_K1E_THREADS=256"],
     "exact_batch0": ["-DDBAG_K1E_BATCH=0", "-DDBAG_K1E_LEAN=0"],
+    "exact_batch32": ["-DDBAG_K1E_BATCH=32"],
+    "exact_batch128": ["-DDBAG_K1E_BATCH=128"],
     "exact_lean0": ["-DDBAG_K1E_LEAN=0"],
     "exact_prefetch": ["-DDBAG_K1E_PREFETCH=1", "-DDBAG_K1E_LEAN=0"],
     "exact_mdiv0": ["-DDBAG_K1E_MDIV=0"],
