@@ -13,30 +13,47 @@ namespace exact {
 constexpr double kDampingInit = 1e-4;  // local_opt.cpp:13
 constexpr double kDampingMax = 1e12;   // local_opt.cpp:14
 
-// Same algorithm and constants as oracle.cpp det_sincos.
+// Same algorithm and constants as oracle.cpp det_sincos. With DBAG_SINCOS_CONST
+// the constants sit in constant memory, so each DMUL / DADD takes them as a
+// c[] operand instead of materializing them with uniform moves (same values,
+// same operations, same bits).
+#ifndef DBAG_SINCOS_CONST
+#define DBAG_SINCOS_CONST 1
+#endif
+#if DBAG_SINCOS_CONST
+__constant__ double kSinCosC[20] = {
+    1.5707963267341256,     6.077100506303966e-11,   2.0222662487959506e-21, 0.6366197723675814,
+    2.8114572543455206e-15, -7.647163731819816e-13,  1.6059043836821613e-10, -2.505210838544172e-08,
+    2.7557319223985893e-06, -0.0001984126984126984,  0.008333333333333333,   -0.16666666666666666,
+    -1.5619206968586225e-16, 4.779477332387385e-14,  -1.1470745597729725e-11, 2.08767569878681e-09,
+    -2.755731922398589e-07, 2.48015873015873e-05,    -0.001388888888888889,  0.041666666666666664};
+#define DBAG_SC(i, v) kSinCosC[i]
+#else
+#define DBAG_SC(i, v) (v)
+#endif
 __device__ __forceinline__ void det_sincos(double x, double* sn, double* cs) {
-  const double kH1 = 1.5707963267341256, kH2 = 6.077100506303966e-11,
-               kH3 = 2.0222662487959506e-21, kTwoOverPi = 0.6366197723675814;
+  const double kH1 = DBAG_SC(0, 1.5707963267341256), kH2 = DBAG_SC(1, 6.077100506303966e-11),
+               kH3 = DBAG_SC(2, 2.0222662487959506e-21), kTwoOverPi = DBAG_SC(3, 0.6366197723675814);
   const double k = rint(x * kTwoOverPi);
   const double r = ((x - k * kH1) - k * kH2) - k * kH3;
   const double z = r * r;
-  double p = 2.8114572543455206e-15;
-  p = p * z + -7.647163731819816e-13;
-  p = p * z + 1.6059043836821613e-10;
-  p = p * z + -2.505210838544172e-08;
-  p = p * z + 2.7557319223985893e-06;
-  p = p * z + -0.0001984126984126984;
-  p = p * z + 0.008333333333333333;
-  p = p * z + -0.16666666666666666;
+  double p = DBAG_SC(4, 2.8114572543455206e-15);
+  p = p * z + DBAG_SC(5, -7.647163731819816e-13);
+  p = p * z + DBAG_SC(6, 1.6059043836821613e-10);
+  p = p * z + DBAG_SC(7, -2.505210838544172e-08);
+  p = p * z + DBAG_SC(8, 2.7557319223985893e-06);
+  p = p * z + DBAG_SC(9, -0.0001984126984126984);
+  p = p * z + DBAG_SC(10, 0.008333333333333333);
+  p = p * z + DBAG_SC(11, -0.16666666666666666);
   const double s = r + (r * z) * p;
-  double q = -1.5619206968586225e-16;
-  q = q * z + 4.779477332387385e-14;
-  q = q * z + -1.1470745597729725e-11;
-  q = q * z + 2.08767569878681e-09;
-  q = q * z + -2.755731922398589e-07;
-  q = q * z + 2.48015873015873e-05;
-  q = q * z + -0.001388888888888889;
-  q = q * z + 0.041666666666666664;
+  double q = DBAG_SC(12, -1.5619206968586225e-16);
+  q = q * z + DBAG_SC(13, 4.779477332387385e-14);
+  q = q * z + DBAG_SC(14, -1.1470745597729725e-11);
+  q = q * z + DBAG_SC(15, 2.08767569878681e-09);
+  q = q * z + DBAG_SC(16, -2.755731922398589e-07);
+  q = q * z + DBAG_SC(17, 2.48015873015873e-05);
+  q = q * z + DBAG_SC(18, -0.001388888888888889);
+  q = q * z + DBAG_SC(19, 0.041666666666666664);
   const double hz = 0.5 * z;
   const double w = 1.0 - hz;
   const double c = w + (((1.0 - w) - hz) + (z * z) * q);
