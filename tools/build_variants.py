@@ -33,6 +33,7 @@ VARIANTS = {
     "exact_rolltrig0": ["-DDBAG_K1E_ROLLTRIG=0"],
     "exact_rcpfast0": ["-DDBAG_K1E_RCPFAST=0"],
     "exact_sinconst0": ["-DDBAG_SINCOS_CONST=0"],
+    "exact_finmax0": ["-DDBAG_K1E_FINMAX=0"],
     "exact_jacinline0": ["-DDBAG_K1E_JACINLINE=0"],
     "exact_lean2_0": ["-DDBAG_K1E_LEAN2=0"],
     "exact_lean3_0": ["-DDBAG_K1E_LEAN3=0"],
