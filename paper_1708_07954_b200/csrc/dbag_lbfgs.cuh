@@ -208,7 +208,7 @@ __device__ __noinline__ bool local_lbfgs(const DevState& S, const HuberProblem& 
 }
 
 #ifndef DBAG_K1_HUB_MINB
-#define DBAG_K1_HUB_MINB 1
+#define DBAG_K1_HUB_MINB 3  // 168 regs: 149.8 ms; minBlocks 1 lets ptxas take ~255 regs (186 ms)
 #endif
 __global__ void __launch_bounds__(kHuberThreads, DBAG_K1_HUB_MINB) k_local_huber(DevState S, int64_t begin,
                                                                int64_t count) {
