@@ -775,15 +775,15 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent4(DevStat
       const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
       const double y0 = (c11 * a0 - c01 * a1) * idet;
       const double y1 = (c00 * a1 - c01 * a0) * idet;
-      bool fin = true;
+      unsigned ex = 0;  // any non-finite step component: exponent field 0x7ff
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
         const double dk = u[k] - iD[k] * (sc[k * 128] * y0 + sc[(9 + k) * 128] * y1);
-        fin = fin && isfinite(dk);
+        ex = max(ex, (unsigned)__double2hiint(dk) & 0x7ff00000u);
         d2 += dk * dk;
         vt[k] = (k == 0 ? v0 : k == 1 ? v1 : k == 2 ? v2 : VC(k - 3)) + dk;
       }
-      proj = fin;
+      proj = ex != 0x7ff00000u;
     } else {
       vt[0] = v0;
       vt[1] = v1;
@@ -798,8 +798,11 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent4(DevStat
       double Rt[9], wt[3], et0 = 0.0, et1 = 0.0, objt = 0.0;
       P.z0 = Z0;
       P.z1 = Z1;
-      const bool ok = gn_residual(P, vt, trt, Rt, wt, et0, et1, objt) && isfinite(et0) &&
-                      isfinite(et1) && isfinite(objt);
+      const bool feas = gn_residual(P, vt, trt, Rt, wt, et0, et1, objt);
+      const unsigned ex = max(max((unsigned)__double2hiint(et0) & 0x7ff00000u,
+                                  (unsigned)__double2hiint(et1) & 0x7ff00000u),
+                              (unsigned)__double2hiint(objt) & 0x7ff00000u);
+      const bool ok = feas && ex != 0x7ff00000u;
       bool take = false;
       if (fresh) {
         if (ok) {
