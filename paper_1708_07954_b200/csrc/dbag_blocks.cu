@@ -314,12 +314,14 @@ __device__ __forceinline__ double objective_rows(const Blk& k, const Carve& c, c
 }
 
 __device__ __forceinline__ bool weight_rows_finite(const Blk& k, const Carve& c, const double* V) {
-  bool ok = true;
+  // all rows finite iff the largest exponent field stays below 0x7ff (inf and
+  // NaN are exactly that field): independent rows, no short-circuit chain
+  unsigned ex = 0;
   for (int i = 0; i < k.D; ++i) {
     const double w = i < k.cb ? k.wx : k.wy;
-    ok = ok && isfinite(w * (V[i] - c.tgt[i]));
+    ex = max(ex, (unsigned)__double2hiint(w * (V[i] - c.tgt[i])) & 0x7ff00000u);
   }
-  return ok;
+  return ex != 0x7ff00000u;
 }
 
 __device__ __forceinline__ double seq_dot(const double* a, const double* b, int n) {
