@@ -737,8 +737,9 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
   h_value<kT>(S, k, c, c.v, c.r, &c.red[0]);
   h_grad<kT>(S, k, c, c.v, c.g);
   if (gtid<kT>() == 0) {
-    bool ok = c.flag[0] == 0 && c.flag[1] == 0 && isfinite(c.red[0]);
-    for (int i = 0; i < D; ++i) ok = ok && isfinite(c.g[i]);
+    unsigned ex = 0;  // exponent-field max: 0x7ff iff some component is inf / NaN
+    for (int i = 0; i < D; ++i) ex = max(ex, (unsigned)__double2hiint(c.g[i]) & 0x7ff00000u);
+    const bool ok = c.flag[0] == 0 && c.flag[1] == 0 && isfinite(c.red[0]) && ex != 0x7ff00000u;
     c.flag[2] = ok ? 0 : 1;
     ++cnt[0];
     cnt[5] += 450ull * k.nobs + 14ull * D;
@@ -814,8 +815,9 @@ __device__ __forceinline__ bool block_lbfgs(const DevState& S, const Blk& k, con
     gsync<kT>();
     h_grad<kT>(S, k, c, c.vt, c.hdg);  // g_new in hdg
     if (gtid<kT>() == 0) {
-      bool fin = c.flag[1] == 0;
-      for (int i = 0; i < D; ++i) fin = fin && isfinite(c.hdg[i]);
+      unsigned ex = 0;
+      for (int i = 0; i < D; ++i) ex = max(ex, (unsigned)__double2hiint(c.hdg[i]) & 0x7ff00000u);
+      const bool fin = c.flag[1] == 0 && ex != 0x7ff00000u;
       c.flag[5] = fin;
       if (fin) {
         ++cnt[0];
