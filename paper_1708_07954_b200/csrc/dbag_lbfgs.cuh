@@ -97,8 +97,12 @@ __device__ __noinline__ bool local_lbfgs(const DevState& S, const HuberProblem& 
   hub_grad(P, v, tr, R, w, e0, e1, g);
   ++cnt.n_jac;
 #pragma unroll
-  for (int k = 0; k < 9; ++k)
-    if (!isfinite(g[k])) return false;
+  {
+    unsigned ex = 0;  // exponent-field max: 0x7ff iff some component is inf / NaN
+#pragma unroll
+    for (int k = 0; k < 9; ++k) ex = max(ex, (unsigned)__double2hiint(g[k]) & 0x7ff00000u);
+    if (ex == 0x7ff00000u) return false;
+  }
   double hs[DBAG_MAX_LBFGS_MEMORY][9], hy[DBAG_MAX_LBFGS_MEMORY][9], hrho[DBAG_MAX_LBFGS_MEMORY];
   int h_first = 0, h_size = 0;  // ring buffer: oldest at h_first
   double gamma = 1.0;
@@ -157,10 +161,10 @@ __device__ __noinline__ bool local_lbfgs(const DevState& S, const HuberProblem& 
     double gt[9];
     hub_grad(P, xt, trt, Rt, wt, et0, et1, gt);
     ++cnt.n_jac;
-    bool gfin = true;
+    unsigned gex = 0;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) gfin = gfin && isfinite(gt[k]);
-    if (!gfin) return true;  // kLineSearchFailed
+    for (int k = 0; k < 9; ++k) gex = max(gex, (unsigned)__double2hiint(gt[k]) & 0x7ff00000u);
+    if (gex == 0x7ff00000u) return true;  // kLineSearchFailed
     ++cnt.n_acc;
     double s[9], y[9];
 #pragma unroll
