@@ -502,3 +502,38 @@ def test_branch_free_reciprocal_is_ieee():
     import paper_1708_07954_b200.admm as A
     for seed in (1, 2, 3):
         assert A.selftest_division(1 << 26, seed) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rho", [1e250, 1e-250])
+def test_out_of_band_solves_take_the_exact_fallback(O, P, rho):
+    """With rho far outside [2^-400, 2^400] every LDLT pivot, target division and
+    diagonal solve of K1 leaves the Markstein band, so every damped solve runs the
+    out-of-line IEEE path (dbag_exact.cu ldlt_solve_slow) and every refill the
+    '/' targets: still bit-identical to the oracle."""
+    arrays, init = orbit_arrays(O, 93, 0.01, 0.01)
+    oprob, osol, g = pair(O, P, arrays, init, rho_x=rho, rho_y=rho, max_iters=4)
+    ref = P.ParamState(arrays[0], arrays[1], arrays[2])
+    ot = osol.run(arrays[0], arrays[2])
+    gt = g.run(ref)
+    assert_exact_trajectory(ot, gt)
+    assert_state_identical(osol, g)
+
+
+@pytest.mark.gpu
+def test_pivot_ties_take_the_exact_fallback(O, P):
+    """Focal lengths of 1e-200 make the projection Jacobian's squares underflow to
+    zero, so every H_ii is exactly w^2: a nine-way tie in the pivot search that
+    the key sort cannot certify, and the exact selection loop (pivot_order_call)
+    decides every order (the zero multipliers then also send the solve out of
+    line). Bit-identical."""
+    arrays, init = orbit_arrays(O, 100, 0.05, 0.2)
+    cam_pose, cam_f, points, cam, pt, uv = arrays
+    f0 = np.full_like(cam_f, 1e-200)
+    arrays0 = (cam_pose, f0, points, cam, pt, uv)
+    oprob, osol, g = pair(O, P, arrays0, init, max_iters=4)
+    ref = P.ParamState(cam_pose, f0, points)
+    ot = osol.run(cam_pose, points)
+    gt = g.run(ref)
+    assert_exact_trajectory(ot, gt)
+    assert_state_identical(osol, g)
