@@ -213,3 +213,16 @@ def test_block_trajectory_config_scenes(O, P, config, scale, ppb, cpb, loss):
     for _ in range(4):
         assert_same_record(osol.iterate(), gsol.iterate())
     assert_same_state(osol, gsol)
+
+
+@pytest.mark.parametrize("ppb,cpb", [(8, 1), (4, 2)])
+def test_block_pivot_ties_take_the_exact_fallback(O, P, ppb, cpb):
+    """Focal lengths of 1e-200 make every H_ii exactly w^2 (the Jacobian's squares
+    underflow), a D-way tie the parallel pivot order cannot certify: the selection
+    loop decides (dbag_blocks.cu pivot_order_par fallback). Bit-identical."""
+    s, ip, ix = scene(O, 83, n_cameras=9, n_points=40, visibility_window=4)
+    s.cam_f[:] = 1e-200
+    osol, gsol = pair(O, P, s, ip, ix, ppb, cpb)
+    for _ in range(3):
+        assert_same_record(osol.iterate(), gsol.iterate())
+        assert_same_state(osol, gsol)
