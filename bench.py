@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -423,6 +424,23 @@ def our_arm(args, rank, world, local_rank):
                          f"(local+consensus+dual), oracle/ restatement (reference needs "
                          f"Eigen3, absent)"}
 
+    # The reference's IterationRecord carries +inf when any consensus point
+    # projects at depth <= eps (admm_solver.cpp:437-460). The bench line must stay
+    # strict JSON, so a non-finite value becomes null, plus the first offending
+    # pair from the throwing variant (problem.cpp mean_reprojection_error).
+    last_round = {k: last[k] for k in ("iter", "mean_reproj_err", "max_primal_x",
+                                       "max_primal_y", "max_dual_x", "max_dual_y")}
+    if rank == 0 and not math.isfinite(last_round["mean_reproj_err"]):
+        last_round["mean_reproj_err"] = None
+        last_round["mean_reproj_err_note"] = "non-finite"
+        try:
+            if world == 1:
+                solver.mean_reprojection_error()
+        except P.admm.DepthBelowGuard as e:
+            last_round["mean_reproj_err_note"] = (
+                f"+inf per the reference's rule: consensus point {e.point_id} at depth "
+                f"{e.depth:.3g} <= eps in camera {e.cam_id} (first offender)")
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -443,8 +461,7 @@ def our_arm(args, rank, world, local_rank):
             "gpu_launches": (6 if world > 1 else 5) * args.steps,
             "counters": {k: stats[k] for k in ("n_jacobian", "n_trial", "n_accept",
                                                "n_direction", "n_pairs_used")},
-            "last_round": {k: last[k] for k in ("iter", "mean_reproj_err", "max_primal_x",
-                                                "max_primal_y", "max_dual_x", "max_dual_y")},
+            "last_round": last_round,
         }
         print(json.dumps(line), flush=True)
     solver.close()
