@@ -171,6 +171,17 @@ def cpu_sample_for(scene, loss, workers, budget_s, blocks=(1, 1)):
     return sample_problem(scene, int(max(4000, budget_s / max(per_obs_s, 1e-9))))
 
 
+def _finite(x):
+    """Strict JSON for the driver: any non-finite float becomes null."""
+    if isinstance(x, dict):
+        return {k: _finite(v) for k, v in x.items()}
+    if isinstance(x, (list, tuple)):
+        return [_finite(v) for v in x]
+    if isinstance(x, float) and not math.isfinite(x):
+        return None
+    return x
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
@@ -194,7 +205,7 @@ def reference_arm(args, rank, world):
                                    f"timed scope local+consensus+dual (admm_solver.cpp:438-443)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(_finite(line), allow_nan=False), flush=True)
     return 0
 
 
@@ -463,7 +474,7 @@ def our_arm(args, rank, world, local_rank):
                                                "n_direction", "n_pairs_used")},
             "last_round": last_round,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line), allow_nan=False), flush=True)
     solver.close()
     if world > 1:
         torch.distributed.destroy_process_group()
