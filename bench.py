@@ -128,18 +128,27 @@ def measured_peaks():
         return {}
 
 
-def sample_problem(scene, target_obs):
-    """Bounded sample of the same workload: cameras [0, C) and every
-    observation of them (points renumbered). Returns arrays for the oracle."""
+def scene_dict(scene):
+    """The product's Scene as the plain arrays the oracle legs take (the same
+    keys oracle.generate_config_scene returns)."""
     p = scene.problem
-    counts = np.bincount(p.obs_cam, minlength=p.num_cameras)
+    return dict(obs_cam=p.obs_cam, obs_pt=p.obs_pt, obs_uv=p.obs_uv, cam_pose=p.cam_pose,
+                cam_f=p.cam_f, points=p.points, init_pose=scene.init.cam_pose,
+                init_pts=scene.init.points)
+
+
+def sample_arrays(d, target_obs):
+    """Bounded sample of a scene: cameras [0, C) and every observation of
+    them (points renumbered). Returns arrays for the oracle."""
+    m = len(d["cam_f"])
+    counts = np.bincount(d["obs_cam"], minlength=m)
     cum = np.cumsum(counts)
-    C = int(min(p.num_cameras, max(1, np.searchsorted(cum, target_obs) + 1)))
-    sel = p.obs_cam < C
-    pts, inv = np.unique(p.obs_pt[sel], return_inverse=True)
-    return dict(cam_pose=p.cam_pose[:C], cam_f=p.cam_f[:C], points=p.points[pts],
-                obs_cam=p.obs_cam[sel], obs_pt=inv.astype(np.int32), obs_uv=p.obs_uv[sel],
-                init_pose=scene.init.cam_pose[:C], init_pts=scene.init.points[pts],
+    C = int(min(m, max(1, np.searchsorted(cum, target_obs) + 1)))
+    sel = d["obs_cam"] < C
+    pts, inv = np.unique(d["obs_pt"][sel], return_inverse=True)
+    return dict(cam_pose=d["cam_pose"][:C], cam_f=d["cam_f"][:C], points=d["points"][pts],
+                obs_cam=d["obs_cam"][sel], obs_pt=inv.astype(np.int32), obs_uv=d["obs_uv"][sel],
+                init_pose=d["init_pose"][:C], init_pts=d["init_pts"][pts],
                 cameras=C, l=int(sel.sum()))
 
 
@@ -147,8 +156,7 @@ def oracle_rounds(sample, loss, workers, rounds, warmup=0, blocks=(1, 1)):
     """Runs the CPU restatement of the reference (oracle/) on the sample;
     returns per-round wall_ms in the reference's own timed scope
     (local+consensus+dual, admm_solver.cpp:438-443)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
+    O = oracle_module()
     op = O.Problem.create(sample["cam_pose"], sample["cam_f"], sample["points"],
                           sample["obs_cam"], sample["obs_pt"], sample["obs_uv"])
     solver = O.AdmmSolver(op, sample["init_pose"], sample["cam_f"], sample["init_pts"],
@@ -163,12 +171,12 @@ def oracle_rounds(sample, loss, workers, rounds, warmup=0, blocks=(1, 1)):
     return ms
 
 
-def cpu_sample_for(scene, loss, workers, budget_s, blocks=(1, 1)):
+def cpu_sample_for(d, loss, workers, budget_s, blocks=(1, 1)):
     """Size a sample so one oracle round takes about budget_s on `workers`."""
-    probe = sample_problem(scene, 4000)
+    probe = sample_arrays(d, 4000)
     ms = oracle_rounds(probe, loss, workers, 2, blocks=blocks)
     per_obs_s = (max(ms) / 1e3) / probe["l"]
-    return sample_problem(scene, int(max(4000, budget_s / max(per_obs_s, 1e-9))))
+    return sample_arrays(d, int(max(4000, budget_s / max(per_obs_s, 1e-9))))
 
 
 def _finite(x):
@@ -182,28 +190,51 @@ def _finite(x):
     return x
 
 
+def oracle_module():
+    """The CPU restatement of the reference (oracle/, test infrastructure). Only
+    bench.py's CPU legs load it, never the product path."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    return O
+
+
 def reference_arm(args, rank, world):
+    """The reference's own CPU path, on the box's host cores, over the SAME
+    workload the GPU arm times: the whole config scene (every observation),
+    ADMM rounds 1..K from the same initial estimate, in the reference's own
+    timed scope (local+consensus+dual; admm_solver.cpp:438-443, the scope
+    `dba bench` reports, dba_main.cpp:327-360). The reference needs Eigen3,
+    which is absent here, so it runs the oracle/ restatement (bit-identical
+    trajectory to the GPU's EXACT mode). The scene comes from the config
+    generator compiled into liboracle.so: this process never loads the
+    product library. The W warm-up rounds run on a small sample of the scene
+    (untimed; they warm the worker pool and the allocator), so the timed
+    rounds are rounds 1..K exactly as on the GPU."""
     if rank != 0:
         return 0
-    import paper_1708_07954_b200 as P
-    scene = P.generate_config_scene(args.config, args.seed)
+    O = oracle_module()
+    d = O.generate_config_scene(args.config, args.seed)
     workers = os.cpu_count() or 1
-    budget = max(0.05, min(2.0, 150.0 / max(1, args.steps + args.warmup)))
-    sample = cpu_sample_for(scene, args.loss, workers, budget, blocks(args))
-    ms = oracle_rounds(sample, args.loss, workers, args.steps, args.warmup, blocks(args))
+    m, n, L = len(d["cam_f"]), len(d["points"]), len(d["obs_cam"])
+    warm = sample_arrays(d, 20000)
+    oracle_rounds(warm, args.loss, workers, 0, args.warmup, blocks(args))
+    ms = oracle_rounds(dict(d, l=L), args.loss, workers, args.steps, 0, blocks(args))
     total_s = sum(ms) / 1e3
-    value = sample["l"] * args.steps / total_s
+    value = L * args.steps / total_s
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, DESIGN.md §Inputs)",
-        "config": config_block(args, scene),
+        "config": config_block(args, m, n, L),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"cameras [0,{sample['cameras']}) of the scene, "
-                                   f"{sample['l']} observations, one ADMM round per step, "
-                                   f"timed scope local+consensus+dual (admm_solver.cpp:438-443)"},
+                         "sample": f"the whole scene ({L} observations, {m} cameras, {n} points), "
+                                   f"ADMM rounds 1..{args.steps} from the generator's initial "
+                                   f"estimate, timed scope local+consensus+dual "
+                                   f"(admm_solver.cpp:438-443); warm-up: {args.warmup} rounds "
+                                   f"on a {warm['l']}-observation sample"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "round_ms": ms,
     }
     print(json.dumps(_finite(line), allow_nan=False), flush=True)
     return 0
@@ -213,13 +244,11 @@ def blocks(args):
     return (args.points_per_block, args.cameras_per_block)
 
 
-def config_block(args, scene):
-    p = scene.problem
+def config_block(args, m, n, L):
     return {"workload": CONFIG_NAMES[args.config], "config_id": args.config,
             "block_config": {"points_per_block": args.points_per_block,
                              "cameras_per_block": args.cameras_per_block},
-            "cameras": int(p.num_cameras), "points": int(p.num_points),
-            "observations": int(p.num_observations), "loss": args.loss,
+            "cameras": int(m), "points": int(n), "observations": int(L), "loss": args.loss,
             "numerics": args.numerics,
             "rounds_per_solve": args.steps, "seed": args.seed,
             "l2_flush": "not needed: per-round state > 126 MB L2",
@@ -426,7 +455,7 @@ def our_arm(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         workers = os.cpu_count() or 1
-        sample = cpu_sample_for(scene, args.loss, workers, 3.0, blocks(args))
+        sample = cpu_sample_for(scene_dict(scene), args.loss, workers, 3.0, blocks(args))
         ms = oracle_rounds(sample, args.loss, workers, 3, blocks=blocks(args))
         cpu = {"value": sample["l"] * 3 / (sum(ms) / 1e3), "unit": UNIT, "cores": workers,
                "kind": "port",
@@ -459,7 +488,7 @@ def our_arm(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "strong",  # total work (config 5) fixed as N grows
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, DESIGN.md §Inputs)",
-            "config": config_block(args, scene),
+            "config": config_block(args, p.num_cameras, p.num_points, L),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                     "d2h_bytes_per_step": d2h / args.steps,
                     "scope": f"dbag_create (H2D + device index build) + {args.steps} rounds "

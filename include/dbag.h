@@ -158,7 +158,9 @@ int dbag_consensus_update(dbag_solver* h);           /* consensus_update() */
 int dbag_dual_update(dbag_solver* h);                /* dual_update()      */
 
 /* Reference state for the MSE columns of iterate()/run() (the reference
- * passes `const ParamState*` per call, admm_solver.hpp:97-100). NULL clears. */
+ * passes `const ParamState*` per call, admm_solver.hpp:97-100). NULL clears.
+ * Always the GLOBAL state ([m][6], [n][3]); a sharded handle keeps its own
+ * cameras and points of it. */
 int dbag_set_reference(dbag_solver* h, const dbag_param_view* ref);
 /* iterate(const ParamState*) (admm_solver.cpp:437-460); with_reference != 0
  * fills camera_mse/point_mse against the dbag_set_reference state. */
@@ -192,7 +194,14 @@ int dbag_get_blocks(dbag_solver* h, int64_t* obs_off, int64_t* pt_off, int32_t* 
                     int64_t* cam_off, int32_t* cam_ids, int32_t* obs_pt_local,
                     int32_t* obs_cam_local);
 
-/* Result/objective queries (admm_solver.hpp:110-127). */
+/* Result/objective queries (admm_solver.hpp:110-127).
+ * dbag_max_primal: max_primal_residual_points/cameras (admm_solver.cpp:359-383),
+ *   one device pass. On a sharded handle: the maximum over this rank's copies
+ *   (the reference's value is the maximum over the ranks).
+ * dbag_dual_sums: dual_sum_point/camera (admm_solver.cpp:385-399) for every
+ *   point and camera, in GLOBAL indexing. On a sharded handle: the sums over
+ *   this rank's copies, zero where the rank holds no copy (the reference's
+ *   sums are the element-wise sum over the ranks). */
 int dbag_max_primal(dbag_solver* h, double* max_x, double* max_y);
 int dbag_dual_sums(dbag_solver* h, double* point_sums /*[n][3]*/, double* cam_sums /*[m][6]*/);
 int dbag_block_objective(dbag_solver* h, int64_t block, double* out);
@@ -276,7 +285,8 @@ int dbag_attach_nccl(dbag_solver* h, const uint8_t id[128]);
  *   exchange_copy(dst, src, 0) for every (dst, src) pair
  *   phase 1: point consensus/dual/metric + partial metrics
  *   exchange_copy(dst, src, 1) for every pair
- *   phase 2: combine -> *out (only for phase 2; may be NULL otherwise). */
+ *   phase 2: combine -> *out (only for phase 2; may be NULL otherwise).
+ * The MSE columns are filled when a reference is set (dbag_set_reference). */
 int dbag_round_phase(dbag_solver* h, int32_t phase, dbag_iteration_record* out);
 int dbag_exchange_copy(dbag_solver* dst, dbag_solver* src, int32_t which);
 

@@ -756,6 +756,13 @@ void WorkerPool::worker_loop() {
       if (stop_) return;
       seen = generation_;
       fn = fn_;
+      // A worker that wakes after run() has already finished this generation
+      // sees fn_ == nullptr. Entering the grab loop then would race the next
+      // run()'s reset of next_/total_ and call through a null (or dangling)
+      // function pointer; it must go back to waiting instead. (The reference's
+      // parallel.cpp:63-91 has the same window; fixing it changes no numerics:
+      // every index is still run exactly once by someone.)
+      if (fn == nullptr) continue;
       ++active_;
     }
     for (;;) {

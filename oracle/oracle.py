@@ -324,6 +324,41 @@ def perturb(pose, f, pts, sigma_cam, sigma_point, seed):
     return po, xo
 
 
+class ConfigSceneInfo(C.Structure):
+    """dbag_scene_info (include/dbag.h)."""
+    _fields_ = [("config", C.c_int32), ("seed", C.c_uint64), ("scale", C.c_double),
+                ("num_cameras", C.c_int32), ("num_points", C.c_int32), ("num_obs", C.c_int64),
+                ("sigma_pixel", C.c_double), ("outlier_frac", C.c_double),
+                ("sigma_init", C.c_double)]
+
+
+def generate_config_scene(config, seed=0, scale=1.0):
+    """BASELINE.json configs 1-5, built by the copy of the config
+    generator compiled into liboracle.so (oracle/Makefile), so a CPU-only
+    process (bench.py --impl reference) never loads the product library.
+    Returns a dict of numpy arrays: obs_cam, obs_pt, obs_uv, cam_pose (ground
+    truth), cam_f, points (ground truth), init_pose, init_pts."""
+    L = lib()
+    h = C.c_void_p()
+    info = ConfigSceneInfo()
+    rc = L.dbag_scene_generate(C.c_int32(config), C.c_uint64(seed), C.c_double(scale),
+                               C.byref(h), C.byref(info))
+    if rc != 0:
+        raise OracleError(f"config scene generation failed ({rc})", rc)
+    try:
+        m, n, l = info.num_cameras, info.num_points, info.num_obs
+        d = {"obs_cam": np.zeros(l, np.int32), "obs_pt": np.zeros(l, np.int32),
+             "obs_uv": np.zeros((l, 2)), "cam_pose": np.zeros((m, 6)), "cam_f": np.zeros(m),
+             "points": np.zeros((n, 3)), "init_pose": np.zeros((m, 6)),
+             "init_pts": np.zeros((n, 3))}
+        L.dbag_scene_fetch(h, _p(d["obs_cam"], IPTR), _p(d["obs_pt"], IPTR), _p(d["obs_uv"]),
+                           _p(d["cam_pose"]), _p(d["cam_f"]), _p(d["points"]),
+                           _p(d["init_pose"]), _p(d["init_pts"]))
+    finally:
+        L.dbag_scene_destroy(h)
+    return d
+
+
 def rng_draw(seed, kind, count, arg=0):
     out = np.zeros(count)
     lib().orc_rng_draw(C.c_ulonglong(seed), kind, C.c_ulonglong(arg), count, _p(out))

@@ -378,9 +378,6 @@ __device__ __forceinline__ void pivot_order(const Blk& k, const Carve& c) {
   }
 }
 
-#ifndef DBAG_GEN_PARPIV
-#define DBAG_GEN_PARPIV 1
-#endif
 // The same pivot order in parallel, verified: every thread ranks its
 // variables by |hd| (descending, ties by index) and scatters them. The
 // selection loop yields exactly that order when the sorted values are
@@ -426,26 +423,12 @@ __device__ __forceinline__ void pivot_order_par(const Blk& k, const Carve& c) {
 // Result in c.dl. Scratch: c.dl / c.vt (temp[] double buffer), c.hdg is kept.
 __device__ __forceinline__ int rowp(int i) { return i * (i + 1) / 2; }
 
-#ifndef DBAG_GEN_COLMAJOR
-#define DBAG_GEN_COLMAJOR 0  // measured slower at (32,1): 43.3 vs 39.1 ms per round, config 2
-#endif
-#if DBAG_GEN_COLMAJOR
-// M packed by columns: column j holds rows j..D-1 contiguously, so a warp's
-// lanes (consecutive rows) read consecutive doubles (no bank conflicts).
-__device__ __forceinline__ int colp(int j, int D) { return j * D - j * (j - 1) / 2; }
-__device__ __forceinline__ int mix(int i, int j, int D) { return colp(j, D) + i - j; }
-#else
 __device__ __forceinline__ int mix(int i, int j, int D) { return rowp(i) + j; }
-#endif
 
 template <int kT, bool kSharedM>
 __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double* M) {
   const int D = k.D;
-#if DBAG_GEN_PARPIV
   pivot_order_par<kT>(k, c);
-#else
-  pivot_order<kT>(k, c);
-#endif
   gsync<kT>();
   const int ne = rowp(D);
   for (int e = gtid<kT>(); e < ne; e += kT) {
@@ -469,17 +452,8 @@ __device__ __forceinline__ void ldlt_solve(const Blk& k, const Carve& c, double*
     if (kk > 0) {
       for (int i = kk + gtid<kT>(); i < D; i += kT) {
         double s = 0.0;
-#if DBAG_GEN_COLMAJOR
-        int a = i;  // mix(i, 0)
-#pragma unroll 4
-        for (int j = 0; j < kk; ++j) {
-          s += M[a] * tc[j];
-          a += D - j - 1;  // mix(i, j + 1) - mix(i, j)
-        }
-#else
         const double* Mi = M + rowp(i);
         for (int j = 0; j < kk; ++j) s += Mi[j] * tc[j];
-#endif
         M[mix(i, kk, D)] = M[mix(i, kk, D)] - s;
       }
       gsync<kT>();
@@ -1005,6 +979,7 @@ __global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(
 // ---- camera consensus / dual over copies (admm_solver.cpp:333-355) --------
 constexpr int kGCamThreads = 128;
 __global__ void __launch_bounds__(kGCamThreads) k_gen_cameras(DevState S, GenState G, int mode) {
+  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
   __shared__ double ybs[6];
   __shared__ double red[kGCamThreads / 32];
   const int j = blockIdx.x;
@@ -1071,6 +1046,7 @@ __global__ void __launch_bounds__(kGCamThreads) k_gen_cameras(DevState S, GenSta
 constexpr int kGPtThreads = 256;
 __global__ void __launch_bounds__(kGPtThreads) k_gen_points(DevState S, GenState G, int mode,
                                                             int metric) {
+  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
   __shared__ double smem[(kGPtThreads / 32) * 2];
   const int64_t tix = (int64_t)blockIdx.x * kGPtThreads + threadIdx.x;
   double err_sum = 0.0, worst = 0.0, dual_res = 0.0, infeasible = 0.0;

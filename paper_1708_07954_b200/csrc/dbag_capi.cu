@@ -27,18 +27,6 @@
 
 using namespace dbag;
 
-#ifndef DBAG_EFFORT_ORDER
-#define DBAG_EFFORT_ORDER 1  // Huber K1 in last-round effort order (launch_local)
-#endif
-#ifndef DBAG_FAST_V4
-#define DBAG_FAST_V4 1  // k_local_persistent4 (Jacobian after accept, state in shared memory)
-#endif
-#ifndef DBAG_FAST_V3
-#define DBAG_FAST_V3 1  // k_local_persistent3 (unified projection, CTA phase barrier)
-#endif
-#ifndef DBAG_FAST_PERSIST
-#define DBAG_FAST_PERSIST 1  // FAST GN: persistent lane-refill K1 (dbag_local.cuh)
-#endif
 
 namespace {
 
@@ -239,38 +227,20 @@ struct dbag_solver {
       return;
     }
     if (exact()) {
-      CK(exact::launch_local(opts.loss == DBAG_LOSS_HUBER && !exact::huber_persistent()
+      CK(exact::launch_local(opts.loss == DBAG_LOSS_HUBER
                                  ? effort_order(begin, count)
                                  : S,
                              begin, count, stream));
       return;
     }
     if (opts.loss == DBAG_LOSS_SQUARED_L2) {
-#if DBAG_FAST_PERSIST
-#if DBAG_FAST_V4
       auto* kern = k_local_persistent4;
       const size_t smem = kFast4Smem;
-#elif DBAG_FAST_V3
-      auto* kern = k_local_persistent3;
-      const size_t smem = kFast3Smem;
-#else
-      auto* kern = k_local_persistent2;
-      const size_t smem = kFastPersistSmem;
-#endif
-      static int resident = 0;
-      if (resident == 0) {
-        int sms = 0, per_sm = 0;
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
-        resident = sms * (per_sm > 0 ? per_sm : 1);
-      }
+      int resident = 0;
+      CK(resident_ctas((const void*)kern, 128, smem, &resident));
       CK(cudaMemsetAsync(S.work, 0, sizeof(unsigned long long), stream));
       const int64_t g = (int64_t)grid_for(count, 128);
       kern<<<(unsigned)(g < resident ? g : resident), 128, smem, stream>>>(S, begin, count);
-#else
-      k_local<0><<<grid_for(count, 128), 128, 0, stream>>>(S, begin, count);
-#endif
       CK_LAUNCH();
       return;
     }
@@ -315,7 +285,9 @@ struct dbag_solver {
     CK(cudaEventRecord(e[0], stream));
     launch_local(0, num_blocks());
     CK(cudaEventRecord(e[1], stream));
+    S.gate = S.err_block;
     launch_camera(kModeConsensus | kModeDual);
+    S.gate = nullptr;
     if (sharded() && S.send_count > 0) {
       k_pack_send<<<grid_for(S.send_count, 256), 256, 0, stream>>>(S);
       CK_LAUNCH();
@@ -324,7 +296,9 @@ struct dbag_solver {
   }
   // Phase 1: point consensus+dual+metric, MSE, this rank's partial record.
   void phase1(cudaEvent_t* e, bool with_ref) {
+    S.gate = S.err_block;
     launch_point(kModeConsensus | kModeDual, true);
+    S.gate = nullptr;
     CK(cudaEventRecord(e[3], stream));
     if (with_ref) {
       k_mse<<<n_mse_parts, 256, 0, stream>>>(S);
@@ -600,7 +574,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     S.work = dev_alloc<unsigned long long>(pool, 1);
     S.effort = nullptr;
     S.order = nullptr;
-    if (opts->loss == DBAG_LOSS_HUBER && DBAG_EFFORT_ORDER) {
+    if (opts->loss == DBAG_LOSS_HUBER) {
       // effort-ordered Huber K1 (launch_local): per-observation effort, the
       // order it sorts into, and the sort's buffers
       S.effort = dev_alloc<uint16_t>(pool, L);
@@ -912,13 +886,10 @@ int dbag_round_phase(dbag_solver* h, int32_t phase, dbag_iteration_record* out) 
     if (phase == 0) {
       h->phase0(e);
     } else if (phase == 1) {
-      h->phase1(e, false);
+      h->phase1(e, h->has_ref);
     } else if (phase == 2) {
-      if (!h->sharded()) {
-        // a single-GPU solver combines its own partial
-      }
       h->phase2(e);
-      if (out) h->fill_record(out, false);
+      if (out) h->fill_record(out, h->has_ref);
       else ++h->iteration;
     } else {
       raise(DBAG_ERR_VALIDATION, "phase must be 0, 1 or 2");
@@ -993,15 +964,29 @@ int dbag_set_reference(dbag_solver* h, const dbag_param_view* ref) {
       h->has_ref = false;
       return;
     }
-    if (ref->num_cameras != h->S.M || ref->num_points != h->S.N)
+    // The reference is the GLOBAL state (as dbag_set_consensus takes it); a
+    // shard keeps its cameras [cam_begin, cam_begin + M) and its local points.
+    if (ref->num_cameras != h->M_total || ref->num_points != h->N_total)
       raise(DBAG_ERR_SIZE_MISMATCH, "state and reference sizes differ");
     if (!h->S.ref_pose) {
       h->S.ref_pose = dev_alloc<double>(h->pool, 6 * (size_t)h->S.M);
       h->S.ref_pts = dev_alloc<double>(h->pool, 3 * (size_t)h->S.N);
     }
-    CK(cudaMemcpyAsync(h->S.ref_pose, ref->cam_pose, sizeof(double) * 6 * h->S.M,
+    std::vector<double> pose, pts;
+    const double* src_pose = ref->cam_pose;
+    const double* src_pts = ref->points;
+    if (h->sharded()) {
+      pose.assign(ref->cam_pose + 6 * (size_t)h->cam_begin,
+                  ref->cam_pose + 6 * ((size_t)h->cam_begin + h->S.M));
+      pts.resize(3 * (size_t)h->S.N);
+      for (int32_t i = 0; i < h->S.N; ++i)
+        for (int k = 0; k < 3; ++k) pts[3 * (size_t)i + k] = ref->points[3 * (size_t)h->local_points[i] + k];
+      src_pose = pose.data();
+      src_pts = pts.data();
+    }
+    CK(cudaMemcpyAsync(h->S.ref_pose, src_pose, sizeof(double) * 6 * h->S.M,
                        cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemcpyAsync(h->S.ref_pts, ref->points, sizeof(double) * 3 * h->S.N,
+    CK(cudaMemcpyAsync(h->S.ref_pts, src_pts, sizeof(double) * 3 * h->S.N,
                        cudaMemcpyHostToDevice, h->stream));
     h->sync();
     h->has_ref = true;
@@ -1262,34 +1247,22 @@ int dbag_max_primal(dbag_solver* h, double* max_x, double* max_y) {
       *max_y = o[1];
       return;
     }
-    // primal-only pass: camera and point kernels in dual mode on a scratch copy
-    // would mutate duals; instead evaluate directly.
+    // (1,1): one device pass over the copies in local indexing. On a sharded
+    // handle this is the maximum over this rank's copies; the reference's
+    // global value is the maximum over the ranks (include/dbag.h).
     const DevState& S = h->S;
-    std::vector<double> lp(3 * S.L), lc(6 * S.L), r(3 * S.L), s(6 * S.L);
-    if (copies_io(h, lp.data(), lc.data(), r.data(), s.data(), 0) != DBAG_OK)
-      raise(DBAG_ERR_CUDA, g_err);
-    std::vector<double> pose(6 * (size_t)S.M), pts(3 * (size_t)S.N);
-    if (dbag_get_consensus(h, pose.data(), nullptr, pts.data()) != DBAG_OK)
-      raise(DBAG_ERR_CUDA, g_err);
-    std::vector<int32_t> bc(S.L), bp(S.L);
-    CK(cudaMemcpy(bc.data(), S.blk_cam, 4 * S.L, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(bp.data(), S.blk_pt, 4 * S.L, cudaMemcpyDeviceToHost));
-    double wx = 0.0, wy = 0.0;
-    for (int64_t b = 0; b < S.L; ++b) {
-      double a = 0.0, c = 0.0;
-      for (int k = 0; k < 3; ++k) {
-        const double d = lp[3 * b + k] - pts[3 * (size_t)bp[b] + k];
-        a += d * d;
-      }
-      for (int k = 0; k < 6; ++k) {
-        const double d = lc[6 * b + k] - pose[6 * (size_t)bc[b] + k];
-        c += d * d;
-      }
-      wx = std::max(wx, std::sqrt(a));
-      wy = std::max(wy, std::sqrt(c));
+    auto* d = reinterpret_cast<unsigned long long*>(S.record + kRecFields);
+    CK(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), h->stream));
+    if (S.L > 0) {
+      const int64_t g = std::min<int64_t>(grid_for(S.L, 256), 148 * 8);
+      k_max_primal<<<(unsigned)g, 256, 0, h->stream>>>(S, d);
+      CK_LAUNCH();
     }
-    *max_x = wx;
-    *max_y = wy;
+    double o[2];
+    CK(cudaMemcpyAsync(o, d, sizeof(o), cudaMemcpyDeviceToHost, h->stream));
+    h->sync();
+    *max_x = o[0];
+    *max_y = o[1];
   });
 }
 
@@ -1305,11 +1278,28 @@ int dbag_dual_sums(dbag_solver* h, double* point_sums, double* cam_sums) {
       k_dual_sums<<<grid_for((int64_t)S.N + S.M, 128), 128, 0, h->stream>>>(S, d, d + 3 * (size_t)S.N);
       CK_LAUNCH();
     }
-    CK(cudaMemcpyAsync(point_sums, d, sizeof(double) * 3 * S.N, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaMemcpyAsync(cam_sums, d + 3 * (size_t)S.N, sizeof(double) * 6 * S.M,
-                       cudaMemcpyDeviceToHost, h->stream));
+    if (!h->sharded()) {
+      CK(cudaMemcpyAsync(point_sums, d, sizeof(double) * 3 * S.N, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaMemcpyAsync(cam_sums, d + 3 * (size_t)S.N, sizeof(double) * 6 * S.M,
+                         cudaMemcpyDeviceToHost, h->stream));
+      h->sync();
+      cudaFree(d);
+      return;
+    }
+    // Sharded: the sums over THIS rank's copies, scattered to global indices
+    // (the caller's buffers are global-sized; entries this rank does not hold
+    // are zero). The reference's sums are the element-wise sum over ranks.
+    std::vector<double> loc(3 * (size_t)S.N + 6 * (size_t)S.M);
+    CK(cudaMemcpyAsync(loc.data(), d, sizeof(double) * loc.size(), cudaMemcpyDeviceToHost, h->stream));
     h->sync();
     cudaFree(d);
+    std::fill(point_sums, point_sums + 3 * (size_t)h->N_total, 0.0);
+    std::fill(cam_sums, cam_sums + 6 * (size_t)h->M_total, 0.0);
+    for (int32_t i = 0; i < S.N; ++i)
+      for (int k = 0; k < 3; ++k) point_sums[3 * (size_t)h->local_points[i] + k] = loc[3 * (size_t)i + k];
+    for (int32_t j = 0; j < S.M; ++j)
+      for (int k = 0; k < 6; ++k)
+        cam_sums[6 * ((size_t)h->cam_begin + j) + k] = loc[3 * (size_t)S.N + 6 * (size_t)j + k];
   });
 }
 

@@ -5,7 +5,44 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace dbag {
+
+// Launch configuration of a persistent kernel on the CURRENT device: opts the
+// kernel in to `smem` bytes of dynamic shared memory (the attribute applies to
+// the current device only) and returns the resident CTA count (SMs x CTAs per
+// SM). Cached per (kernel, device, threads, smem) under a mutex, so solvers on
+// several devices or threads each get their own; every CUDA error is returned.
+inline cudaError_t resident_ctas(const void* kern, int threads, size_t smem, int* out) {
+  static std::mutex mu;
+  static std::map<std::pair<std::pair<const void*, int>, std::pair<int, size_t>>, int> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(std::make_pair(kern, dev), std::make_pair(threads, smem));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  int sms = 0, per_sm = 0;
+  if (smem > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+          cudaSuccess)
+    return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+    return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem)) !=
+      cudaSuccess)
+    return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  *out = cache[key] = sms * per_sm;
+  return cudaSuccess;
+}
 
 // Point-side per-copy record, stored in POINT-MAJOR order (copies of one point
 // contiguous, ascending camera = ascending block order, admm_solver.cpp:126-140).
@@ -53,6 +90,11 @@ struct DevState {
   double* part_mse;       // [gridMSE][2]
   unsigned long long* counters;  // [kCounterStripes][8]
   int64_t* err_block;     // first block that raised (local_update_all)
+  // Inside a fused round (iterate/run/enqueue_round) = err_block: the
+  // consensus/dual kernels return at once when the round's local solve raised,
+  // as the reference's local_update_all throws before consensus_update and
+  // dual_update run (admm_solver.cpp:292-316, 437-443). Null otherwise.
+  const int64_t* gate;
   int64_t* err_obs;       // first infeasible observation (input order)
   double* record;         // DevRecord
   double* metric_part;    // [kRecFields] this rank's partial record (raw sums)

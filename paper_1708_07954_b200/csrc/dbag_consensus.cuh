@@ -35,6 +35,7 @@ __device__ __forceinline__ void write_camR(const DevState& S, int j, const doubl
 // K3: one CTA per camera segment [cam_off[j], cam_off[j+1]) of block order.
 template <int MODE>
 __global__ void __launch_bounds__(kCamThreads) k_camera(DevState S) {
+  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
   __shared__ double smem[(kCamThreads / 32) * 6];
   __shared__ double ybar_s[6];
   const int j = blockIdx.x;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kCamThreads) k_camera(DevState S) {
 // the point-major record array.
 template <int MODE, bool kMetric>
 __global__ void __launch_bounds__(kPtThreads) k_point(DevState S) {
+  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
   __shared__ double smem[(kPtThreads / 32) * 2];
   const int64_t t = (int64_t)blockIdx.x * kPtThreads + threadIdx.x;
   double err_sum = 0.0, worst = 0.0, dual_res = 0.0, infeasible = 0.0;
@@ -425,6 +427,45 @@ __global__ void k_dual_sums(DevState S, double* pts, double* cams) {
     for (int64_t b = S.cam_off[j]; b < S.cam_off[j + 1]; ++b)
       for (int k = 0; k < 6; ++k) a[k] += S.cam_soa[(int64_t)(6 + k) * S.L + b];
     for (int k = 0; k < 6; ++k) cams[6 * (int64_t)j + k] = a[k];
+  }
+}
+
+// max_primal_residual_points/cameras (admm_solver.cpp:359-383): max over this
+// solver's copies of ||copy - consensus||_2, in LOCAL indexing (a shard's
+// blk_pt/blk_cam index its own xbar/ybar). The squared norm is summed in the
+// reference's component order with explicit _rn operations (this TU is built
+// with FMA contraction on). std::max(worst, v) ignores a NaN v; inf counts.
+// Non-negative doubles order like their bit patterns, so a 64-bit atomicMax
+// per CTA gives the same value in any order. out[0..1] start at +0.
+__global__ void k_max_primal(DevState S, unsigned long long* out) {
+  unsigned long long wx = 0, wy = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < S.L;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const PointRec& rec = S.prec[S.blk_pos[b]];
+    const double4 xb = S.xbar[S.blk_pt[b]];
+    const double d0 = __dsub_rn(rec.x0, xb.x), d1 = __dsub_rn(rec.x1, xb.y),
+                 d2 = __dsub_rn(rec.x2, xb.z);
+    double a = 0.0;
+    a = __dadd_rn(a, __dmul_rn(d0, d0));
+    a = __dadd_rn(a, __dmul_rn(d1, d1));
+    a = __dadd_rn(a, __dmul_rn(d2, d2));
+    const double* yb = S.ybar + 8 * (int64_t)S.blk_cam[b];
+    double c = 0.0;
+    for (int k = 0; k < 6; ++k) {
+      const double d = __dsub_rn(S.cam_soa[(int64_t)k * S.L + b], yb[k]);
+      c = __dadd_rn(c, __dmul_rn(d, d));
+    }
+    const double va = __dsqrt_rn(a), vc = __dsqrt_rn(c);
+    if (va == va) wx = max(wx, (unsigned long long)__double_as_longlong(va));
+    if (vc == vc) wy = max(wy, (unsigned long long)__double_as_longlong(vc));
+  }
+  for (int o = 16; o; o >>= 1) {
+    wx = max(wx, __shfl_xor_sync(0xffffffffu, wx, o));
+    wy = max(wy, __shfl_xor_sync(0xffffffffu, wy, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, wx);
+    atomicMax(out + 1, wy);
   }
 }
 

@@ -14,7 +14,6 @@ cudaError_t launch_camera(const DevState& S, int mode, cudaStream_t st);
 cudaError_t launch_point(const DevState& S, int mode, bool metric, int n_parts, cudaStream_t st);
 cudaError_t launch_camR_all(const DevState& S, cudaStream_t st);
 // the Huber K1 is the persistent lane-refill kernel (block order, no effort sort)
-bool huber_persistent();
 // test hook: count n branch-free reciprocals that differ bitwise from IEEE 1/d
 cudaError_t selftest_rcp(int64_t n, unsigned long long seed, unsigned long long* bad_dev);
 }  // namespace exact

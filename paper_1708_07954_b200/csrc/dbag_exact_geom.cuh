@@ -17,10 +17,6 @@ constexpr double kDampingMax = 1e12;   // local_opt.cpp:14
 // the constants sit in constant memory, so each DMUL / DADD takes them as a
 // c[] operand instead of materializing them with uniform moves (same values,
 // same operations, same bits).
-#ifndef DBAG_SINCOS_CONST
-#define DBAG_SINCOS_CONST 1
-#endif
-#if DBAG_SINCOS_CONST
 __constant__ double kSinCosC[20] = {
     1.5707963267341256,     6.077100506303966e-11,   2.0222662487959506e-21, 0.6366197723675814,
     2.8114572543455206e-15, -7.647163731819816e-13,  1.6059043836821613e-10, -2.505210838544172e-08,
@@ -28,9 +24,6 @@ __constant__ double kSinCosC[20] = {
     -1.5619206968586225e-16, 4.779477332387385e-14,  -1.1470745597729725e-11, 2.08767569878681e-09,
     -2.755731922398589e-07, 2.48015873015873e-05,    -0.001388888888888889,  0.041666666666666664};
 #define DBAG_SC(i, v) kSinCosC[i]
-#else
-#define DBAG_SC(i, v) (v)
-#endif
 __device__ __forceinline__ void det_sincos(double x, double* sn, double* cs) {
   const double kH1 = DBAG_SC(0, 1.5707963267341256), kH2 = DBAG_SC(1, 6.077100506303966e-11),
                kH3 = DBAG_SC(2, 2.0222662487959506e-21), kTwoOverPi = DBAG_SC(3, 0.6366197723675814);

@@ -115,562 +115,14 @@ __device__ __forceinline__ void proj_jacobian(const double v[9], const Trig& t, 
   A1[8] = b1;
 }
 
-// gauss_newton (local_opt.cpp:20-82) on the 11-row residual. Returns false if
-// the residual is undefined at the start (the reference throws).
-__device__ __forceinline__ bool local_gn(const DevState& S, const GnProblem& P, double v[9],
-                                         LocalCounters& cnt) {
-  Trig tr;
-  double R[9], w[3], e0, e1, obj;
-  if (!gn_residual(P, v, tr, R, w, e0, e1, obj) || !isfinite(e0) || !isfinite(e1) ||
-      !isfinite(obj))
-    return false;
-  const double wx2 = P.wx * P.wx, wy2 = P.wy * P.wy;
-  const double iwx2 = 1.0 / wx2, iwy2 = 1.0 / wy2;  // D^-1 of the undamped first trial
-  for (int it = 0; it < S.inner_max_iters; ++it) {
-    // J = [-A ; diag(w)] at v
-    double A0[9], A1[9];
-    proj_jacobian(v, tr, R, w, P.f, A0, A1);
-    ++cnt.n_jac;
-    double rhs[9], g2 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      const double wk = k < 3 ? P.wx : P.wy;
-      const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.T(k)));
-      rhs[k] = -jtr;                 // -0.5 g
-      const double gk = 2.0 * jtr;   // g = 2 J^T r
-      g2 += gk * gk;
-    }
-    if (sqrt(g2) <= S.grad_tol) return true;  // kGradConverged
-    double lambda = 0.0;
-    for (;;) {
-      // (A^T A + D) delta = rhs, D_k = w_k^2 + lambda*max(H_kk, 1e-12)
-      double iD[9], u[9];
-      double c00 = 1.0, c01 = 0.0, c11 = 1.0, a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const double wk2 = k < 3 ? wx2 : wy2;
-        if (lambda > 0.0) {
-          const double hkk = (A0[k] * A0[k] + A1[k] * A1[k]) + wk2;
-          iD[k] = fast_rcp(wk2 + lambda * fmax(hkk, 1e-12));
-        } else {
-          iD[k] = k < 3 ? iwx2 : iwy2;
-        }
-        u[k] = rhs[k] * iD[k];
-        c00 += A0[k] * A0[k] * iD[k];
-        c01 += A0[k] * A1[k] * iD[k];
-        c11 += A1[k] * A1[k] * iD[k];
-        a0 += A0[k] * u[k];
-        a1 += A1[k] * u[k];
-      }
-      const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
-      const double y0 = (c11 * a0 - c01 * a1) * idet;
-      const double y1 = (c00 * a1 - c01 * a0) * idet;
-      double vt[9], d2 = 0.0;
-      bool fin = true;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const double dk = u[k] - iD[k] * (A0[k] * y0 + A1[k] * y1);
-        fin = fin && isfinite(dk);
-        d2 += dk * dk;
-        vt[k] = v[k] + dk;
-      }
-      if (fin) {
-        Trig trt;
-        double Rt[9], wt[3], et0, et1, objt;
-        ++cnt.n_trial;
-        if (gn_residual(P, vt, trt, Rt, wt, et0, et1, objt) && isfinite(et0) && isfinite(et1) &&
-            isfinite(objt) && objt <= obj) {
-          ++cnt.n_acc;
-#pragma unroll
-          for (int k = 0; k < 9; ++k) v[k] = vt[k];
-#pragma unroll
-          for (int k = 0; k < 9; ++k) R[k] = Rt[k];
-          tr = trt;
-          w[0] = wt[0];
-          w[1] = wt[1];
-          w[2] = wt[2];
-          e0 = et0;
-          e1 = et1;
-          obj = objt;
-          double x2 = 0.0;
-#pragma unroll
-          for (int k = 0; k < 9; ++k) x2 += v[k] * v[k];
-          if (sqrt(d2) <= S.step_tol * (1.0 + sqrt(x2))) return true;  // kStepConverged
-          break;
-        }
-      }
-      lambda = lambda == 0.0 ? kDampingInit : lambda * 10.0;
-      if (lambda > kDampingMax) return true;  // kLineSearchFailed / kSingularSystem
-    }
-  }
-  return true;  // kMaxIters
-}
-
 #ifndef DBAG_K1_MINB
 #define DBAG_K1_MINB 4  // 128 regs: 16 warps/SM beat spill-free 8 warps (84 -> 67 ms, config 5)
 #endif
 
-// K1 entry: blocks [begin, begin+count) in block order.
-template <int kLoss>
-__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local(DevState S, int64_t begin, int64_t count) {
-  __shared__ double tgt_s[9 * 128];
-  const int64_t b = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  LocalCounters cnt;
-  if (b < begin + count) {
-    const int32_t j = S.blk_cam[b];
-    const int32_t i = S.blk_pt[b];
-    const int32_t p = S.blk_pos[b];
-    const double* yb = S.ybar + 8 * (int64_t)j;
-    const double4 xb = S.xbar[i];
-    const PointRec rec = S.prec[p];
-    double v[9], sd[6];
-    v[0] = rec.x0;
-    v[1] = rec.x1;
-    v[2] = rec.x2;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      v[3 + k] = S.cam_soa[(int64_t)k * S.L + b];
-      sd[k] = S.cam_soa[(int64_t)(6 + k) * S.L + b];
-    }
-    bool ok;
-    if (kLoss == 0) {
-      GnProblem P;
-      P.tgt = tgt_s + threadIdx.x;
-      // completed-square targets x~ = xbar - r/rho, y~ = ybar - s/rho (:152-164)
-      P.tgt[0] = xb.x - rec.r0 / S.rho_x;
-      P.tgt[128] = xb.y - rec.r1 / S.rho_x;
-      P.tgt[256] = xb.z - rec.r2 / S.rho_x;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) P.tgt[(3 + k) * 128] = yb[k] - sd[k] / S.rho_y;
-      P.z0 = rec.u;
-      P.z1 = rec.v;
-      P.f = yb[6];
-      P.wx = sqrt(0.5 * S.rho_x);  // :183-184
-      P.wy = sqrt(0.5 * S.rho_y);
-      P.eps = S.eps_depth;
-      ok = local_gn(S, P, v, cnt);
-    } else {
-      ok = false;  // Huber path: see dbag_lbfgs.cuh (k_local<1> specialisation)
-    }
-    if (!ok) {
-      atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)b);
-    } else {
-      double* xp = reinterpret_cast<double*>(S.prec + p);
-      xp[0] = v[0];
-      xp[1] = v[1];
-      xp[2] = v[2];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) S.cam_soa[(int64_t)k * S.L + b] = v[3 + k];
-    }
-  }
-  flush_counters(S, cnt);
-}
-
-
-// gauss_newton (local_opt.cpp:20-82) as a persistent per-lane state machine
-// (the FAST K1 for squared L2): one loop iteration = (Jacobian if the lane
-// needs one) + one trial; a lane whose observation finished refills from the
-// global work counter, so warps stay full although observations need very
-// different numbers of iterations and damping retries (k_local keeps ~12/32
-// lanes busy, profiles/). The Jacobian rows A0|A1, rhs and H_kk live in the
-// thread's shared slice (formed once per GN iteration, read by every damping
-// trial), R is recomputed from the trig values instead of held, and the refill
-// issues its loads first: 59.9 -> 52.5 ms at config 5 against k_local (a first
-// persistent version that held that state in registers lost, 57.6 -> 70.2 ms).
-// 45 doubles of shared memory per thread with the targets.
-constexpr int kFastScr = 36;
-constexpr size_t kFastPersistSmem = sizeof(double) * (9 + kFastScr) * 128;
-
-__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent2(DevState S, int64_t begin,
-                                                                         int64_t count) {
-  extern __shared__ double fp_dyn[];
-  LocalCounters cnt;
-  GnProblem P;
-  P.tgt = fp_dyn + threadIdx.x;
-  double* sc = fp_dyn + 9 * 128 + threadIdx.x;  // A0 0..8 | A1 9..17 | rhs 18..26 | H_kk 27..35
-  P.wx = sqrt(0.5 * S.rho_x);  // admm_solver.cpp:183-184
-  P.wy = sqrt(0.5 * S.rho_y);
-  P.eps = S.eps_depth;
-  const double wx2 = P.wx * P.wx, wy2 = P.wy * P.wy;
-  const double iwx2 = 1.0 / wx2, iwy2 = 1.0 / wy2;  // D^-1 of the undamped trial
-  bool busy = false, need_jac = false, exhausted = false;
-  int64_t b = -1;
-  int it = 0;
-  double lambda = 0.0, obj = 0.0, e0 = 0.0, e1 = 0.0;
-  double v[9], w[3];
-  Trig tr;
-  for (;;) {
-    const int64_t idx = refill(S, !busy, count, exhausted);
-    if (idx >= 0) {
-      b = begin + idx;
-      const int32_t j = S.blk_cam[b];
-      const int32_t i = S.blk_pt[b];
-      const PointRec rec = S.prec[S.blk_pos[b]];
-      const double* yb = S.ybar + 8 * (int64_t)j;
-      const double4 xb = S.xbar[i];
-      double sd[6], yv[7];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        v[3 + k] = S.cam_soa[(int64_t)k * S.L + b];
-        sd[k] = S.cam_soa[(int64_t)(6 + k) * S.L + b];
-      }
-#pragma unroll
-      for (int k = 0; k < 7; ++k) yv[k] = yb[k];
-      v[0] = rec.x0;
-      v[1] = rec.x1;
-      v[2] = rec.x2;
-      P.tgt[0] = xb.x - rec.r0 / S.rho_x;
-      P.tgt[128] = xb.y - rec.r1 / S.rho_x;
-      P.tgt[256] = xb.z - rec.r2 / S.rho_x;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) P.tgt[(3 + k) * 128] = yv[k] - sd[k] / S.rho_y;
-      P.z0 = rec.u;
-      P.z1 = rec.v;
-      P.f = yv[6];
-      double R[9];
-      if (gn_residual(P, v, tr, R, w, e0, e1, obj) && isfinite(e0) && isfinite(e1) &&
-          isfinite(obj)) {
-        busy = true;
-        need_jac = true;
-        it = 0;
-      } else {  // the reference throws (local_opt.cpp:25-28)
-        atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)b);
-      }
-    }
-    if (__ballot_sync(0xffffffffu, busy) == 0) {
-      if (exhausted) break;
-      continue;
-    }
-    bool done = false;
-    if (busy && need_jac) {
-      if (it >= S.inner_max_iters) {
-        done = true;  // kMaxIters
-      } else {
-        double R[9], A0[9], A1[9];
-        rot_of(tr, R);
-        proj_jacobian(v, tr, R, w, P.f, A0, A1);
-        ++cnt.n_jac;
-        double g2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          const double wk = k < 3 ? P.wx : P.wy;
-          const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.T(k)));
-          sc[k * 128] = A0[k];
-          sc[(9 + k) * 128] = A1[k];
-          sc[(18 + k) * 128] = -jtr;  // rhs = -0.5 g
-          sc[(27 + k) * 128] = (A0[k] * A0[k] + A1[k] * A1[k]) + (k < 3 ? wx2 : wy2);
-          const double gk = 2.0 * jtr;  // g = 2 J^T r
-          g2 += gk * gk;
-        }
-        if (sqrt(g2) <= S.grad_tol) {
-          done = true;  // kGradConverged
-        } else {
-          need_jac = false;
-          lambda = 0.0;
-        }
-      }
-    }
-    if (busy && !done && !need_jac) {
-      double iD[9], u[9];
-      double c00 = 1.0, c01 = 0.0, c11 = 1.0, a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const double A0k = sc[k * 128], A1k = sc[(9 + k) * 128];
-        const double wk2 = k < 3 ? wx2 : wy2;
-        iD[k] = lambda > 0.0 ? fast_rcp(wk2 + lambda * fmax(sc[(27 + k) * 128], 1e-12))
-                             : (k < 3 ? iwx2 : iwy2);
-        u[k] = sc[(18 + k) * 128] * iD[k];
-        c00 += A0k * A0k * iD[k];
-        c01 += A0k * A1k * iD[k];
-        c11 += A1k * A1k * iD[k];
-        a0 += A0k * u[k];
-        a1 += A1k * u[k];
-      }
-      const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
-      const double y0 = (c11 * a0 - c01 * a1) * idet;
-      const double y1 = (c00 * a1 - c01 * a0) * idet;
-      double vt[9], d2 = 0.0;
-      bool fin = true;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const double dk = u[k] - iD[k] * (sc[k * 128] * y0 + sc[(9 + k) * 128] * y1);
-        fin = fin && isfinite(dk);
-        d2 += dk * dk;
-        vt[k] = v[k] + dk;
-      }
-      bool accepted = false;
-      if (fin) {
-        Trig trt;
-        double Rt[9], wt[3], et0, et1, objt;
-        ++cnt.n_trial;
-        if (gn_residual(P, vt, trt, Rt, wt, et0, et1, objt) && isfinite(et0) && isfinite(et1) &&
-            isfinite(objt) && objt <= obj) {  // non-strict accept (local_opt.cpp:60)
-          accepted = true;
-          ++cnt.n_acc;
-#pragma unroll
-          for (int k = 0; k < 9; ++k) v[k] = vt[k];
-          tr = trt;
-          w[0] = wt[0];
-          w[1] = wt[1];
-          w[2] = wt[2];
-          e0 = et0;
-          e1 = et1;
-          obj = objt;
-          double x2 = 0.0;
-#pragma unroll
-          for (int k = 0; k < 9; ++k) x2 += v[k] * v[k];
-          if (sqrt(d2) <= S.step_tol * (1.0 + sqrt(x2))) {
-            done = true;  // kStepConverged
-          } else {
-            ++it;
-            need_jac = true;
-          }
-        }
-      }
-      if (!accepted) {
-        lambda = lambda == 0.0 ? kDampingInit : lambda * 10.0;
-        if (lambda > kDampingMax) done = true;
-      }
-    }
-    if (busy && done) {
-      double* xp = reinterpret_cast<double*>(S.prec + S.blk_pos[b]);
-      xp[0] = v[0];
-      xp[1] = v[1];
-      xp[2] = v[2];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) S.cam_soa[(int64_t)k * S.L + b] = v[3 + k];
-      busy = false;
-    }
-  }
-  flush_counters(S, cnt);
-}
-
-
-// FAST L2 K1, v3: the EXACT kernel's structure (dbag_exact.cu) with the FAST
-// arithmetic of k_local_persistent2: one projection per loop iteration shared
-// by a fresh observation's start point and the trial point, the Jacobian
-// after the accept, one CTA barrier per iteration (the warps share the loop
-// body's instruction-cache lines), a warp-local queue of claimed
-// observations, warp-aggregated counters, and the accepted point's trig
-// values and camera-frame point in the shared slice (slots 36..44).
-#ifndef DBAG_K1_SYNC
-#define DBAG_K1_SYNC 0  // phase barrier measured slower for the FAST kernel (49.8 vs 44.4 ms)
-#endif
-constexpr int kFast3Scr = 45;
-constexpr size_t kFast3Smem = sizeof(double) * (9 + kFast3Scr) * 128;
-
-__global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent3(DevState S, int64_t begin,
-                                                                         int64_t count) {
-  extern __shared__ double fp_dyn[];
-  unsigned nj = 0, nt = 0, na = 0;
-  GnProblem P;
-  P.tgt = fp_dyn + threadIdx.x;
-  // A0 0..8 | A1 9..17 | rhs 18..26 | H_kk 27..35 | trig 36..41 | w 42..44
-  double* sc = fp_dyn + 9 * 128 + threadIdx.x;
-  P.wx = S.w_x;  // admm_solver.cpp:183-184
-  P.wy = S.w_y;
-  P.eps = S.eps_depth;
-  const double wx2 = P.wx * P.wx, wy2 = P.wy * P.wy;
-  const double iwx2 = 1.0 / wx2, iwy2 = 1.0 / wy2;  // D^-1 of the undamped trial
-  bool busy = false, need_jac = false, exhausted = false;
-  int64_t b = -1;
-  int it = 0, pos = 0;
-  double lambda = 0.0, obj = 0.0, e0 = 0.0, e1 = 0.0;
-  double v[9];
-  WarpQueue wq;
-  for (;;) {
-    const int64_t idx = refill_batched<64>(S, !busy, count, exhausted, wq);
-    const bool fresh = idx >= 0;
-    if (fresh) {
-      b = begin + idx;
-      const int32_t j = S.blk_cam[b];
-      const int32_t i = S.blk_pt[b];
-      pos = S.blk_pos[b];
-      const PointRec rec = S.prec[pos];
-      const double* yb = S.ybar + 8 * (int64_t)j;
-      const double4 xb = S.xbar[i];
-      double sd[6], yv[7];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        v[3 + k] = S.cam_soa[(int64_t)k * S.L + b];
-        sd[k] = S.cam_soa[(int64_t)(6 + k) * S.L + b];
-      }
-#pragma unroll
-      for (int k = 0; k < 7; ++k) yv[k] = yb[k];
-      v[0] = rec.x0;
-      v[1] = rec.x1;
-      v[2] = rec.x2;
-      P.tgt[0] = xb.x - rec.r0 / S.rho_x;
-      P.tgt[128] = xb.y - rec.r1 / S.rho_x;
-      P.tgt[256] = xb.z - rec.r2 / S.rho_x;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) P.tgt[(3 + k) * 128] = yv[k] - sd[k] / S.rho_y;
-      P.z0 = rec.u;
-      P.z1 = rec.v;
-      P.f = yv[6];
-      busy = true;
-    }
-#if DBAG_K1_SYNC
-    if (!__syncthreads_or(busy)) {
-      if (__syncthreads_and(exhausted)) break;
-      continue;
-    }
-    if (__ballot_sync(0xffffffffu, busy) == 0) continue;
-#else
-    if (__ballot_sync(0xffffffffu, busy) == 0) {
-      if (exhausted) break;
-      continue;
-    }
-#endif
-    bool done = false;
-    // ---- damped solve by Woodbury (see k_local_persistent2)
-    double vt[9], d2 = 0.0;
-    bool proj = fresh;
-    if (busy && !fresh) {
-      double iD[9], u[9];
-      double c00 = 1.0, c01 = 0.0, c11 = 1.0, a0 = 0.0, a1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const double A0k = sc[k * 128], A1k = sc[(9 + k) * 128];
-        const double wk2 = k < 3 ? wx2 : wy2;
-        iD[k] = lambda > 0.0 ? fast_rcp(wk2 + lambda * fmax(sc[(27 + k) * 128], 1e-12))
-                             : (k < 3 ? iwx2 : iwy2);
-        u[k] = sc[(18 + k) * 128] * iD[k];
-        c00 += A0k * A0k * iD[k];
-        c01 += A0k * A1k * iD[k];
-        c11 += A1k * A1k * iD[k];
-        a0 += A0k * u[k];
-        a1 += A1k * u[k];
-      }
-      const double idet = fast_rcp(c00 * c11 - c01 * c01);  // C is SPD, det >= 1
-      const double y0 = (c11 * a0 - c01 * a1) * idet;
-      const double y1 = (c00 * a1 - c01 * a0) * idet;
-      bool fin = true;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const double dk = u[k] - iD[k] * (sc[k * 128] * y0 + sc[(9 + k) * 128] * y1);
-        fin = fin && isfinite(dk);
-        d2 += dk * dk;
-        vt[k] = v[k] + dk;
-      }
-      proj = fin;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 9; ++k) vt[k] = v[k];
-    }
-    // ---- one projection + objective
-    bool accepted = false;
-    if (proj) {
-      Trig trt;
-      double Rt[9], wt[3], et0 = 0.0, et1 = 0.0, objt = 0.0;
-      const bool ok = gn_residual(P, vt, trt, Rt, wt, et0, et1, objt) && isfinite(et0) &&
-                      isfinite(et1) && isfinite(objt);
-      if (fresh || (ok && objt <= obj)) {  // start point / non-strict accept (:60)
-        if (ok) {
-          sc[36 * 128] = trt.sa;
-          sc[37 * 128] = trt.ca;
-          sc[38 * 128] = trt.sb;
-          sc[39 * 128] = trt.cb;
-          sc[40 * 128] = trt.sg;
-          sc[41 * 128] = trt.cg;
-          sc[42 * 128] = wt[0];
-          sc[43 * 128] = wt[1];
-          sc[44 * 128] = wt[2];
-          e0 = et0;
-          e1 = et1;
-          obj = objt;
-        }
-        if (fresh) {
-          if (ok) {
-            need_jac = true;
-            it = 0;
-          } else {  // the reference throws (local_opt.cpp:25-28)
-            atomicMin(reinterpret_cast<unsigned long long*>(S.err_block), (unsigned long long)b);
-            busy = false;
-          }
-        } else {
-          accepted = true;
-          double x2 = 0.0;
-#pragma unroll
-          for (int k = 0; k < 9; ++k) {
-            v[k] = vt[k];
-            x2 += v[k] * v[k];
-          }
-          if (sqrt(d2) <= S.step_tol * (1.0 + sqrt(x2))) {
-            done = true;  // kStepConverged
-          } else {
-            ++it;
-            need_jac = true;
-          }
-        }
-      }
-    }
-    if (busy && !fresh && !accepted) {
-      lambda = lambda == 0.0 ? kDampingInit : lambda * 10.0;
-      if (lambda > kDampingMax) done = true;
-    }
-    nt += __popc(__ballot_sync(0xffffffffu, proj && !fresh));
-    na += __popc(__ballot_sync(0xffffffffu, accepted));
-    bool did_jac = false;
-    // ---- Jacobian and gradient at v
-    if (busy && need_jac && !done) {
-      if (it >= S.inner_max_iters) {
-        done = true;  // kMaxIters
-      } else {
-        Trig tr;
-        tr.sa = sc[36 * 128];
-        tr.ca = sc[37 * 128];
-        tr.sb = sc[38 * 128];
-        tr.cb = sc[39 * 128];
-        tr.sg = sc[40 * 128];
-        tr.cg = sc[41 * 128];
-        const double w[3] = {sc[42 * 128], sc[43 * 128], sc[44 * 128]};
-        double R[9], A0[9], A1[9];
-        rot_of(tr, R);
-        proj_jacobian(v, tr, R, w, P.f, A0, A1);
-        did_jac = true;
-        double g2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          const double wk = k < 3 ? P.wx : P.wy;
-          const double jtr = -(A0[k] * e0 + A1[k] * e1) + wk * (wk * (v[k] - P.T(k)));
-          sc[k * 128] = A0[k];
-          sc[(9 + k) * 128] = A1[k];
-          sc[(18 + k) * 128] = -jtr;  // rhs = -0.5 g
-          sc[(27 + k) * 128] = (A0[k] * A0[k] + A1[k] * A1[k]) + (k < 3 ? wx2 : wy2);
-          const double gk = 2.0 * jtr;  // g = 2 J^T r
-          g2 += gk * gk;
-        }
-        if (sqrt(g2) <= S.grad_tol) {
-          done = true;  // kGradConverged
-        } else {
-          need_jac = false;
-          lambda = 0.0;
-        }
-      }
-    }
-    nj += __popc(__ballot_sync(0xffffffffu, did_jac));
-    if (busy && done) {
-      double* xp = reinterpret_cast<double*>(S.prec + pos);
-      xp[0] = v[0];
-      xp[1] = v[1];
-      xp[2] = v[2];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) S.cam_soa[(int64_t)k * S.L + b] = v[3 + k];
-      busy = false;
-    }
-  }
-  if ((threadIdx.x & 31) == 0) {
-    unsigned long long* slot =
-        S.counters + 8 * ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % kCounterStripes);
-    if (nj) atomicAdd(slot + 0, (unsigned long long)nj);
-    if (nt) atomicAdd(slot + 1, (unsigned long long)nt);
-    if (na) atomicAdd(slot + 2, (unsigned long long)na);
-  }
-}
-
-
-// FAST L2 K1, v4: v3 with the EXACT kernel's later lessons: the Jacobian right
+// FAST L2 K1: a persistent lane-refill state machine with the EXACT kernel's
+// structure (one projection per loop iteration shared by a fresh start point
+// and a trial point, a warp-local queue of claimed observations, warp-
+// aggregated counters) and its later lessons: the Jacobian right
 // after an accept / start point from the residual's trig values, R and w in
 // registers (no accepted-state slots), the warp's index queue and counters in
 // shared memory, and lambda, the objective, the observation and the camera
@@ -739,18 +191,10 @@ __global__ void __launch_bounds__(128, DBAG_K1_MINB) k_local_persistent4(DevStat
       P.f = yb[6];
       busy = true;
     }
-#if DBAG_K1_SYNC
-    if (!__syncthreads_or(busy)) {
-      if (__syncthreads_and(exhausted)) break;
-      continue;
-    }
-    if (__ballot_sync(0xffffffffu, busy) == 0) continue;
-#else
     if (__ballot_sync(0xffffffffu, busy) == 0) {
       if (exhausted) break;
       continue;
     }
-#endif
     bool done = false;
     // ---- damped solve by Woodbury (see k_local_persistent2)
     double vt[9], d2 = 0.0;

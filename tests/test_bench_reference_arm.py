@@ -51,3 +51,23 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1
     d = _strict(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_reference_arm_times_the_whole_scene_without_the_product_library():
+    """The arm's workload is the GPU arm's (every observation of the config,
+    rounds 1..K) and its process never maps libdbag.so."""
+    code = ("import sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', '2', "
+            "'--steps', '2', '--warmup', '3']; import bench; rc = bench.main(); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('PRODUCT_LOADED' if 'libdbag' in maps else 'CLEAN', rc)")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "CLEAN 0" in out.stdout
+    d = _strict([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    scene = O.generate_config_scene(2, 0)
+    assert d["config"]["observations"] == len(scene["obs_cam"])
+    assert d["config"]["cameras"] == 64 and len(d["round_ms"]) == 2
+    assert str(len(scene["obs_cam"])) in d["cpu_baseline"]["sample"]

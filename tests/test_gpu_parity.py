@@ -537,3 +537,56 @@ def test_pivot_ties_take_the_exact_fallback(O, P):
     gt = g.run(ref)
     assert_exact_trajectory(ot, gt)
     assert_state_identical(osol, g)
+
+
+def ragged_arrays(O, P, k):
+    """The first k points of config 1 (8 cameras, all-see-all) with a fixed
+    pattern of observations dropped, so l = 1..~2900 takes sizes that are not
+    multiples of a warp, a CTA or a refill batch. Point 0 keeps all 8
+    observations, so every camera stays covered."""
+    arrays, init, _ = config_arrays(P, 1, 0)
+    cam_pose, cam_f, points, cam, pt, uv = arrays
+    keep = (pt < k) & ((pt == 0) | (cam == pt % 8) | (((pt * 7 + cam * 3) % 5) != 0))
+    return ((cam_pose, cam_f, points[:k], cam[keep], pt[keep], uv[keep]),
+            (init[0], init[1][:k]))
+
+
+@pytest.mark.parametrize("loss", [0, 1])
+def test_ragged_sizes_exact(O, P, loss):
+    """Ragged problem sizes through the persistent lane-refill K1 and the
+    consensus tails (restores the r1 test dropped after the oracle's WorkerPool
+    crash, now fixed: oracle.cpp worker_loop), bit-identical over 8 rounds."""
+    for k in (1, 2, 3, 5, 7, 13, 31, 33, 63, 65, 127, 129, 255, 257, 363, 500):
+        arrays, init = ragged_arrays(O, P, k)
+        _, osol, g = pair(O, P, arrays, init, loss=loss, max_iters=8, workers=16)
+        ot = osol.run()
+        gt = g.run()
+        assert_exact_trajectory(ot, gt)
+        assert_state_identical(osol, g)
+        g.close()
+
+
+@pytest.mark.parametrize("loss", [0, 1])
+def test_local_block_error_leaves_consensus_and_duals(O, P, loss):
+    """A local solve that cannot start (its point copy sits at the camera
+    centre: depth 0 < eps) raises Error("local block N: ...") after every other
+    block finished, and the round's consensus and dual updates do not run
+    (admm_solver.cpp:292-316: local_update_all throws first). The GPU state
+    after the error equals the oracle's bit for bit."""
+    arrays, init = orbit_arrays(O, 93, 0.01, 0.01)
+    _, osol, g = pair(O, P, arrays, init, loss=loss, max_iters=10, workers=1)
+    osol.iterate()
+    g.iterate()
+    lp, lc, r, s = osol.copies()
+    b = len(lp) // 2
+    R = O.rotation_from_euler(*lc[b][:3])
+    lp[b] = -R.T @ lc[b][3:]
+    osol.set_copies(lp, lc, r, s)
+    g.set_copies(lp, lc, r, s)
+    with pytest.raises(O.OracleError) as oe:
+        osol.iterate()
+    with pytest.raises(Exception) as ge:
+        g.iterate()
+    assert f"local block {b}:" in str(oe.value) and f"local block {b}:" in str(ge.value)
+    assert_state_identical(osol, g)
+    g.close()

@@ -79,3 +79,45 @@ def test_sharded_fast_close_to_single(P):
     _, pose, pts = sharded_run(P, scene, opts, 2, 1)
     assert np.allclose(pose, sc.cam_pose, rtol=1e-12, atol=1e-12)
     assert np.allclose(pts, sc.points, rtol=1e-12, atol=1e-12)
+
+
+def test_sharded_queries_and_reference(P):
+    """the queries of a sharded handle. max_primal is the rank-local
+    maximum (its max over ranks is the single-GPU value, bitwise); dual_sums are
+    rank-local sums in GLOBAL indexing (their sum over ranks is the single-GPU
+    sums); set_reference takes the GLOBAL state and the phase rounds then fill
+    the MSE columns like the single-GPU solve."""
+    scene = P.generate_config_scene(5, 4, 0.003)
+    world, rounds = 3, 3
+    opts = P.AdmmOptions(max_iters=rounds)
+    ref = scene.ground_truth
+    single = P.AdmmSolver(scene.problem, scene.init, opts)
+    st = single.run(ref)
+    shards = [P.AdmmSolver.sharded(scene.problem, scene.init, opts, r, world) for r in range(world)]
+    for s in shards:
+        s._use_reference(ref)
+    for _ in range(rounds):
+        for s in shards:
+            s.round_phase(0)
+        for d in shards:
+            for s in shards:
+                d.exchange_copy(s, 0)
+        for s in shards:
+            s.round_phase(1)
+        for d in shards:
+            for s in shards:
+                d.exchange_copy(s, 1)
+        recs = [s.round_phase(2) for s in shards]
+    for k in ("camera_mse", "point_mse"):
+        assert abs(recs[0][k] - st[-1][k]) <= 1e-12 * abs(st[-1][k]), k
+    mx = [s._max_primal() for s in shards]
+    assert max(m[0] for m in mx) == single.max_primal_residual_points()
+    assert max(m[1] for m in mx) == single.max_primal_residual_cameras()
+    assert single.max_primal_residual_points() == st[-1]["max_primal_x"]
+    ps, cs = single.dual_sums()
+    sp = sum(s.dual_sums()[0] for s in shards)
+    sc = sum(s.dual_sums()[1] for s in shards)
+    scale = 1 + max(np.abs(single.state().dual_r).max(), np.abs(single.state().dual_s).max())
+    assert np.abs(sp - ps).max() <= 1e-12 * scale and np.abs(sc - cs).max() <= 1e-12 * scale
+    for s in shards:
+        s.close()
