@@ -241,10 +241,12 @@ int dbag_selftest_division(int32_t device, int64_t n, uint64_t seed, int64_t* mi
 /* ---- multi-GPU ---------------------------------------------
  * Cameras are split into contiguous ranges balanced on observation counts;
  * rank r owns every observation of its cameras. Boundary points (cameras on
- * several ranks) exchange their copies' raw (x, r) through one all-gather per
- * round, so every holder recomputes the reference's sequential consensus sum:
- * the EXACT trajectory is bit-identical for any number of ranks. Host-only
- * plan functions below need no GPU (tested with gloo on CPU). */
+ * several ranks) exchange their copies' raw (x, r) once per round, each copy
+ * only to the other ranks that hold its point (one grouped ncclSend/ncclRecv
+ * pair per peer, no padding), so every holder recomputes the reference's
+ * sequential consensus sum: the EXACT trajectory is bit-identical for any
+ * number of ranks. Host-only plan functions below need no GPU (tested with
+ * gloo on CPU). */
 typedef struct {
   int32_t rank, world;
   int32_t cam_begin, cam_end;   /* this rank's camera range */
@@ -252,7 +254,7 @@ typedef struct {
   int32_t local_points;
   int32_t boundary_points;      /* global */
   int64_t boundary_copies;      /* global */
-  int64_t send_count, max_send; /* this rank's boundary copies; all-gather slot size */
+  int64_t send_count, recv_count; /* this rank's exchange slots per round (48 B each) */
   int64_t comm_floats;          /* reference communication_cost (global) */
 } dbag_shard_info;
 typedef struct dbag_shard_plan dbag_shard_plan;
@@ -263,11 +265,15 @@ int dbag_shard_plan_create(const dbag_problem_view* full, int32_t rank, int32_t 
 void dbag_shard_plan_get_info(const dbag_shard_plan* s, dbag_shard_info* info);
 /* Any pointer may be NULL. Sizes: cam_lo [world+1]; local_obs [local_obs];
  * local_points, bp_of_local, owner_of_local [local_points]; gb_off
- * [boundary_points+1]; gmap [boundary_copies] (recv slot of each global boundary
- * copy); send_obs_local [send_count] (local observation index of each send slot). */
+ * [boundary_points+1]; gmap [boundary_copies]: for a copy of a point this rank
+ * holds, >= 0 its recv slot, -2 - q for this rank's own copy (local observation
+ * q); -1 otherwise; send_obs_local [send_count] (local observation of each
+ * send slot, grouped by destination peer, global copy order within a peer). */
 int dbag_shard_plan_arrays(const dbag_shard_plan* s, int32_t* cam_lo, int64_t* local_obs,
                            int32_t* local_points, int32_t* bp_of_local, int8_t* owner_of_local,
                            int64_t* gb_off, int64_t* gmap, int64_t* send_obs_local);
+/* send_off / recv_off [world+1]: slot ranges per destination / source peer. */
+int dbag_shard_plan_exchange(const dbag_shard_plan* s, int64_t* send_off, int64_t* recv_off);
 void dbag_shard_plan_destroy(dbag_shard_plan* s);
 
 /* A solver for shard `rank` of `world` over the FULL problem/init (every rank
@@ -276,7 +282,8 @@ int dbag_create_sharded(const dbag_problem_view* full, const dbag_param_view* in
                         const dbag_options* opts, int32_t rank, int32_t world,
                         dbag_solver** out);
 /* NCCL transport: rank 0 makes the id, the launcher broadcasts it, every rank
- * attaches; iterate/run/enqueue_round then exchange with ncclAllGather. */
+ * attaches; iterate/run/enqueue_round then exchange the boundary copies with
+ * grouped ncclSend/ncclRecv and the partial records with ncclAllGather. */
 int dbag_nccl_unique_id(uint8_t id[128]);
 int dbag_attach_nccl(dbag_solver* h, const uint8_t id[128]);
 /* External transport (tests, single-device emulation of several ranks): run a

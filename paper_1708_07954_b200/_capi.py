@@ -77,7 +77,7 @@ class ShardInfo(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("cam_begin", C.c_int32),
                 ("cam_end", C.c_int32), ("local_obs", C.c_int64), ("local_points", C.c_int32),
                 ("boundary_points", C.c_int32), ("boundary_copies", C.c_int64),
-                ("send_count", C.c_int64), ("max_send", C.c_int64), ("comm_floats", C.c_int64)]
+                ("send_count", C.c_int64), ("recv_count", C.c_int64), ("comm_floats", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -148,6 +148,7 @@ SIGNATURES = {
                                          C.POINTER(H), C.POINTER(ShardInfo)]),
     "dbag_shard_plan_get_info": (None, [H, C.POINTER(ShardInfo)]),
     "dbag_shard_plan_arrays": (C.c_int, [H, I32P, I64P, I32P, I32P, I8P, I64P, I64P, I64P]),
+    "dbag_shard_plan_exchange": (C.c_int, [H, I64P, I64P]),
     "dbag_shard_plan_destroy": (None, [H]),
     "dbag_create_sharded": (C.c_int, [C.POINTER(ProblemView), C.POINTER(ParamView),
                                       C.POINTER(Options), C.c_int32, C.c_int32, C.POINTER(H)]),

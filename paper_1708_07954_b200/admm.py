@@ -386,7 +386,7 @@ class AdmmSolver:
     shard of a multi-GPU solve (AdmmSolver.sharded)."""
 
     def __init__(self, problem: Problem, init: ParamState, opts: AdmmOptions | None = None,
-                 rank: int = 0, world: int = 1):
+                 rank: int = 0, world: int = 1, sharded: bool = False):
         self._lib = _capi.load()
         self.problem = problem
         self.opts = opts or AdmmOptions()
@@ -394,7 +394,7 @@ class AdmmSolver:
         init = init.copy()
         pv, iv, o = problem._view(), init._view(), self.opts._c()
         self.rank, self.world = rank, world
-        if world == 1:
+        if world == 1 and not sharded:
             _check(self._lib.dbag_create(C.byref(pv), C.byref(iv), C.byref(o), C.byref(self._h)))
         else:
             _check(self._lib.dbag_create_sharded(C.byref(pv), C.byref(iv), C.byref(o), rank, world,
@@ -402,15 +402,16 @@ class AdmmSolver:
         self.m, self.n = problem.num_cameras, problem.num_points
         self.l = problem.num_observations
         self._ref_key = None
-        if world > 1:
+        if world > 1 or sharded:
             self.plan = shard_plan(problem, rank, world)
             info = self.plan["info"]
             self.l = info["local_obs"]  # per-copy state arrays are this shard's
 
     @classmethod
     def sharded(cls, problem, init, opts, rank, world):
-        """Shard `rank` of `world` (cameras split on observation counts)."""
-        return cls(problem, init, opts, rank=rank, world=world)
+        """Shard `rank` of `world` (cameras split on observation counts).
+        world == 1 builds the sharded code path with no peers (one-rank NCCL)."""
+        return cls(problem, init, opts, rank=rank, world=world, sharded=True)
 
     def attach_nccl(self, unique_id: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
@@ -679,13 +680,17 @@ def shard_plan(problem: Problem, rank: int, world: int) -> dict:
                "owner_of_local": np.zeros(d["local_points"], np.int8),
                "gb_off": np.zeros(d["boundary_points"] + 1, np.int64),
                "gmap": np.zeros(d["boundary_copies"], np.int64),
-               "send_obs_local": np.zeros(d["send_count"], np.int64)}
+               "send_obs_local": np.zeros(d["send_count"], np.int64),
+               "send_off": np.zeros(world + 1, np.int64),
+               "recv_off": np.zeros(world + 1, np.int64)}
         p = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
         _check(lib.dbag_shard_plan_arrays(
             h, p(out["cam_lo"], C.c_int32), p(out["local_obs"], C.c_int64),
             p(out["local_points"], C.c_int32), p(out["bp_of_local"], C.c_int32),
             p(out["owner_of_local"], C.c_int8), p(out["gb_off"], C.c_int64),
             p(out["gmap"], C.c_int64), p(out["send_obs_local"], C.c_int64)))
+        _check(lib.dbag_shard_plan_exchange(h, p(out["send_off"], C.c_int64),
+                                            p(out["recv_off"], C.c_int64)))
     finally:
         lib.dbag_shard_plan_destroy(h)
     return out

@@ -146,8 +146,10 @@ struct dbag_solver {
   // shard
   int32_t world = 1, rank = 0, cam_begin = 0;
   std::vector<int32_t> local_points;  // local -> global point id (sharded only)
+  std::vector<int64_t> send_off, recv_off;  // [world+1] exchange slots per peer
   ncclComm_t comm = nullptr;
-  bool sharded() const { return world > 1; }
+  bool shard_mode = false;  // made by dbag_create_sharded (any world, 1 included)
+  bool sharded() const { return shard_mode; }
   // generalized blocks (BlockConfig != {1,1}); null for (1,1)
   std::unique_ptr<blocks::GenSolver> gen;
   // effort-ordered Huber K1 buffers (see effort_order)
@@ -271,12 +273,25 @@ struct dbag_solver {
   void exchange(int which) {
     if (!sharded()) return;
     if (!comm) raise(DBAG_ERR_NCCL, "sharded solver without a transport: dbag_attach_nccl or phases");
-    ncclResult_t r;
-    if (which == 0)
-      r = ncclAllGather(S.send_buf, S.recv_buf, (size_t)S.max_send * 6, ncclDouble, comm, stream);
-    else
-      r = ncclAllGather(S.metric_part, S.metric_recv, kRecFields, ncclDouble, comm, stream);
-    if (r != ncclSuccess) raise(DBAG_ERR_NCCL, std::string("NCCL: ") + ncclGetErrorString(r));
+    auto nck = [](ncclResult_t r) {
+      if (r != ncclSuccess) raise(DBAG_ERR_NCCL, std::string("NCCL: ") + ncclGetErrorString(r));
+    };
+    if (which == 0) {
+      // boundary copies: to each peer exactly the copies of the points it
+      // also holds, one grouped send/recv pair per peer (no padding)
+      nck(ncclGroupStart());
+      for (int32_t q = 0; q < world; ++q) {
+        if (q == rank) continue;
+        const int64_t ns = send_off[q + 1] - send_off[q], nr = recv_off[q + 1] - recv_off[q];
+        if (ns > 0)
+          nck(ncclSend(S.send_buf + 6 * send_off[q], (size_t)ns * 6, ncclDouble, q, comm, stream));
+        if (nr > 0)
+          nck(ncclRecv(S.recv_buf + 6 * recv_off[q], (size_t)nr * 6, ncclDouble, q, comm, stream));
+      }
+      nck(ncclGroupEnd());
+    } else {
+      nck(ncclAllGather(S.metric_part, S.metric_recv, kRecFields, ncclDouble, comm, stream));
+    }
   }
 
   // Phase 0: local solve, camera consensus+dual, pack boundary copies.
@@ -810,7 +825,8 @@ int dbag_create_sharded(const dbag_problem_view* F, const dbag_param_view* init,
     DevState& S = h->S;
     S.world = world;
     S.rank = rank;
-    if (world > 1) {
+    h->shard_mode = true;
+    {
       auto& pool = h->pool;
       cudaStream_t st = h->stream;
       S.bp_of_local = dev_alloc<int32_t>(pool, ln);
@@ -818,12 +834,13 @@ int dbag_create_sharded(const dbag_problem_view* F, const dbag_param_view* init,
       S.gb_off = dev_alloc<int64_t>(pool, plan.gb_off.size());
       S.gmap = dev_alloc<int64_t>(pool, plan.gmap.size());
       S.send_count = plan.send_count;
-      S.max_send = plan.max_send;
+      S.recv_count = plan.recv_count;
+      h->send_off = plan.send_off;
+      h->recv_off = plan.recv_off;
       S.send_pos = dev_alloc<int32_t>(pool, plan.send_count);
-      S.send_buf = dev_alloc<double>(pool, 6 * (size_t)plan.max_send);
-      S.recv_buf = dev_alloc<double>(pool, 6 * (size_t)plan.max_send * world);
+      S.send_buf = dev_alloc<double>(pool, 6 * (size_t)plan.send_count);
+      S.recv_buf = dev_alloc<double>(pool, 6 * (size_t)plan.recv_count);
       S.metric_recv = dev_alloc<double>(pool, (size_t)kRecFields * world);
-      CK(cudaMemsetAsync(S.send_buf, 0, sizeof(double) * 6 * plan.max_send, st));
       CK(cudaMemcpyAsync(S.bp_of_local, plan.bp_of_local.data(), 4 * (size_t)ln,
                          cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(S.owner_of_local, plan.owner_of_local.data(), (size_t)ln,
@@ -833,21 +850,29 @@ int dbag_create_sharded(const dbag_problem_view* F, const dbag_param_view* init,
       if (!plan.gmap.empty())
         CK(cudaMemcpyAsync(S.gmap, plan.gmap.data(), 8 * plan.gmap.size(), cudaMemcpyHostToDevice,
                            st));
+      // local observation -> point-major position, for the send slots and
+      // this rank's own gmap entries
+      int32_t* d_o2b = nullptr;
+      CK(cudaMalloc(&d_o2b, 4 * (size_t)std::max<int64_t>(S.L, 1)));
+      k_obs2blk<<<grid_for(S.L, 256), 256, 0, st>>>(S, d_o2b);
+      CK_LAUNCH();
+      if (!plan.gmap.empty()) {
+        k_gmap_own<<<grid_for((int64_t)plan.gmap.size(), 256), 256, 0, st>>>(
+            S, (int64_t)plan.gmap.size(), d_o2b);
+        CK_LAUNCH();
+      }
       if (plan.send_count > 0) {
         int64_t* d_so = nullptr;
-        int32_t* d_o2b = nullptr;
         CK(cudaMalloc(&d_so, 8 * (size_t)plan.send_count));
-        CK(cudaMalloc(&d_o2b, 4 * (size_t)std::max<int64_t>(S.L, 1)));
         CK(cudaMemcpyAsync(d_so, plan.send_obs_local.data(), 8 * (size_t)plan.send_count,
                            cudaMemcpyHostToDevice, st));
-        k_send_pos<<<grid_for(S.L, 256), 256, 0, st>>>(S, d_so, d_o2b);
-        CK_LAUNCH();
-        k_send_pos2<<<grid_for(plan.send_count, 256), 256, 0, st>>>(S, d_so, d_o2b);
+        k_send_pos<<<grid_for(plan.send_count, 256), 256, 0, st>>>(S, d_so, d_o2b);
         CK_LAUNCH();
         CK(cudaStreamSynchronize(st));
         cudaFree(d_so);
-        cudaFree(d_o2b);
       }
+      CK(cudaStreamSynchronize(st));
+      cudaFree(d_o2b);
       CK(cudaStreamSynchronize(st));
     }
   });
@@ -904,10 +929,16 @@ int dbag_exchange_copy(dbag_solver* dst, dbag_solver* src, int32_t which) {
       raise(DBAG_ERR_VALIDATION, "exchange between solvers of different worlds");
     CK(cudaSetDevice(dst->device));
     if (which == 0) {
-      if (dst->S.max_send != src->S.max_send) raise(DBAG_ERR_VALIDATION, "plan mismatch");
-      const size_t n = (size_t)src->S.max_send * 6;
-      CK(cudaMemcpyAsync(dst->S.recv_buf + n * src->rank, src->S.send_buf, n * sizeof(double),
-                         cudaMemcpyDefault, dst->stream));
+      // src's slots for dst -> dst's slots from src (the same copies, both in
+      // global copy order)
+      if (src == dst) return;
+      const int64_t ns = src->send_off[dst->rank + 1] - src->send_off[dst->rank];
+      const int64_t nr = dst->recv_off[src->rank + 1] - dst->recv_off[src->rank];
+      if (ns != nr) raise(DBAG_ERR_VALIDATION, "plan mismatch");
+      if (ns > 0)
+        CK(cudaMemcpyAsync(dst->S.recv_buf + 6 * dst->recv_off[src->rank],
+                           src->S.send_buf + 6 * src->send_off[dst->rank], 6 * ns * sizeof(double),
+                           cudaMemcpyDefault, dst->stream));
     } else {
       CK(cudaMemcpyAsync(dst->S.metric_recv + (size_t)kRecFields * src->rank, src->S.metric_part,
                          kRecFields * sizeof(double), cudaMemcpyDefault, dst->stream));

@@ -108,15 +108,30 @@ struct DevState {
   int32_t* bp_of_local;   // [N] global boundary index of a local point, or -1
   int8_t* owner_of_local; // [N] 1 if this rank counts the point in point-wise sums
   int64_t* gb_off;        // [B+1] global boundary copy ranges (reference copy order)
-  int64_t* gmap;          // [G] recv slot of each global boundary copy
-  int32_t* send_pos;      // [send_count] point-major position of each send copy
-  int64_t send_count, max_send;
-  double* send_buf;       // [max_send][6] x(3) r(3)
-  double* recv_buf;       // [world * max_send][6]
+  int64_t* gmap;          // [G] per global boundary copy of a point held here: >= 0 its
+                          // recv slot; -2 - p for an own copy at point-major position p
+  int32_t* send_pos;      // [send_count] point-major position of each send slot
+  int64_t send_count, recv_count;
+  double* send_buf;       // [send_count][6] x(3) r(3), grouped by destination peer
+  double* recv_buf;       // [recv_count][6], grouped by source peer
   double* metric_recv;    // [world][kRecFields]
 };
 
 constexpr int kCounterStripes = 64;
+
+// Copy (x, r) of a boundary point from its gmap slot: a peer's copy in the
+// receive buffer, or this rank's own copy in the point-major records.
+__device__ __forceinline__ void boundary_copy(const DevState& S, int64_t slot, double c[6]) {
+  if (slot >= 0) {
+    const double* a = S.recv_buf + 6 * slot;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) c[k] = a[k];
+  } else {
+    const double* a = reinterpret_cast<const double*>(S.prec + (-2 - slot));
+#pragma unroll
+    for (int k = 0; k < 6; ++k) c[k] = a[k];
+  }
+}
 
 // Lane-level work refill for persistent K1 kernels: every idle lane of the
 // warp takes the next observation index (one atomic per warp). Returns the

@@ -119,12 +119,13 @@ __global__ void __launch_bounds__(kPtThreads) k_point(DevState S) {
       const int bp = S.bp_of_local ? S.bp_of_local[i] : -1;
       if (bp >= 0) {
         const int64_t g0 = S.gb_off[bp], g1 = S.gb_off[bp + 1];
-        const double* a = S.recv_buf + 6 * S.gmap[g0];
-        anc[0] = a[0];
-        anc[1] = a[1];
-        anc[2] = a[2];
+        double c[6];
+        boundary_copy(S, S.gmap[g0], c);
+        anc[0] = c[0];
+        anc[1] = c[1];
+        anc[2] = c[2];
         for (int64_t g = g0; g < g1; ++g) {
-          const double* c = S.recv_buf + 6 * S.gmap[g];
+          boundary_copy(S, S.gmap[g], c);
           acc[0] += (c[0] - anc[0]) + inv_rho * c[3];
           acc[1] += (c[1] - anc[1]) + inv_rho * c[4];
           acc[2] += (c[2] - anc[2]) + inv_rho * c[5];
@@ -305,14 +306,22 @@ __global__ void k_pack_send(DevState S) {
   o[5] = r.r2;
 }
 
-// send slot -> point-major position (setup): obs2blk is the inverse of blk_obs.
-__global__ void k_send_pos(DevState S, const int64_t* send_obs_local, int32_t* obs2blk) {
+// Shard setup: local observation -> point-major position for the send slots
+// and for this rank's own entries of gmap (-2 - q -> -2 - position).
+// obs2blk is the inverse of blk_obs.
+__global__ void k_obs2blk(DevState S, int32_t* obs2blk) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b < S.L) obs2blk[S.blk_obs[b]] = (int32_t)b;
 }
-__global__ void k_send_pos2(DevState S, const int64_t* send_obs_local, const int32_t* obs2blk) {
+__global__ void k_send_pos(DevState S, const int64_t* send_obs_local, const int32_t* obs2blk) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s < S.send_count) S.send_pos[s] = S.blk_pos[obs2blk[send_obs_local[s]]];
+}
+__global__ void k_gmap_own(DevState S, int64_t n, const int32_t* obs2blk) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  const int64_t v = S.gmap[g];
+  if (v <= -2) S.gmap[g] = -2 - (int64_t)S.blk_pos[obs2blk[-2 - v]];
 }
 
 // ---- queries ---------------------------------------------------------------

@@ -5,10 +5,12 @@
 // consensus and dual s never leave a rank. A point whose cameras span ranks is
 // a BOUNDARY point. Its copies ("boundary copies", global order = the
 // reference's copy order: by point, then camera — admm_solver.cpp:126-140) are
-// exchanged raw (x and r, 48 B each) with one all-gather per round, so every
-// rank holding the point recomputes the reference's sequential consensus sum
+// exchanged raw (x and r, 48 B each) once per round, each copy only to the
+// other ranks that hold its point (one ncclSend/ncclRecv per peer, grouped), so
+// every holder recomputes the reference's sequential consensus sum
 // (admm_solver.cpp:324-332) bit for bit. Integer and deterministic: every rank
-// derives the same plan from the same full problem.
+// derives the same plan from the same full problem, so a sender's slot order
+// for a peer (global copy order) is the receiver's.
 #include "dbag_shard.h"
 
 #include <algorithm>
@@ -79,29 +81,23 @@ ShardPlan make_shard_plan(int32_t m, int32_t n, int64_t l, const int32_t* cam, c
       bp_of_point[i] = P.n_boundary_points++;
     }
   P.gb_off.assign(P.n_boundary_points + 1, 0);
-  std::vector<int64_t> send_count(world, 0);
   std::vector<int32_t> g_owner;    // per global boundary copy: owning rank
-  std::vector<int64_t> g_pos;      // position in the owner's send buffer
   std::vector<int64_t> g_obs;      // input observation index
   for (int64_t q = 0; q < l; ++q) {
     const int64_t k = order[q];
     const int32_t bp = bp_of_point[pt[k]];
     if (bp < 0) continue;
     ++P.gb_off[bp + 1];
-    const int32_t r = rank_of_cam[cam[k]];
-    g_owner.push_back(r);
-    g_pos.push_back(send_count[r]++);
+    g_owner.push_back(rank_of_cam[cam[k]]);
     g_obs.push_back(k);
   }
   for (int32_t b = 0; b < P.n_boundary_points; ++b) P.gb_off[b + 1] += P.gb_off[b];
   P.n_boundary_copies = (int64_t)g_owner.size();
-  P.max_send = 1;
-  for (int32_t r = 0; r < world; ++r) P.max_send = std::max(P.max_send, send_count[r]);
-  P.send_count = send_count[rank];
-  // recv layout of an all-gather of padded per-rank buffers: rank-major
-  P.gmap.resize(P.n_boundary_copies);
-  for (int64_t g = 0; g < P.n_boundary_copies; ++g)
-    P.gmap[g] = (int64_t)g_owner[g] * P.max_send + g_pos[g];
+  // holders of each boundary point: a bit set over ranks (world <= 64)
+  if (world > 64) throw std::invalid_argument("at most 64 ranks");
+  std::vector<uint64_t> holders(P.n_boundary_points, 0);
+  for (int32_t b = 0; b < P.n_boundary_points; ++b)
+    for (int64_t g = P.gb_off[b]; g < P.gb_off[b + 1]; ++g) holders[b] |= 1ull << g_owner[g];
   // this rank's observations (input order) and local renumbering
   P.cam_begin = P.cam_lo[rank];
   P.cam_end = P.cam_lo[rank + 1];
@@ -133,17 +129,47 @@ ShardPlan make_shard_plan(int32_t m, int32_t n, int64_t l, const int32_t* cam, c
     P.bp_of_local[i] = bp_of_point[g];
     P.owner_of_local[i] = rmin[g] == rank ? 1 : 0;
   }
-  // send list: this rank's boundary copies in global order, as input indices;
-  // the device maps them to its point-major positions
-  for (int64_t g = 0; g < P.n_boundary_copies; ++g)
-    if (g_owner[g] == rank) P.send_obs_local.push_back(-1);
+  // input index -> local observation index
+  std::vector<int64_t> local_index_of_obs(l, -1);
+  for (size_t q = 0; q < P.local_obs.size(); ++q) local_index_of_obs[P.local_obs[q]] = (int64_t)q;
+  // exchange lists, all in global copy order:
+  //  send to peer d: my copies of boundary points d holds;
+  //  recv from peer s: s's copies of boundary points I hold.
+  P.send_off.assign(world + 1, 0);
+  P.recv_off.assign(world + 1, 0);
+  for (int32_t b = 0; b < P.n_boundary_points; ++b)
+    for (int64_t g = P.gb_off[b]; g < P.gb_off[b + 1]; ++g) {
+      const int32_t o = g_owner[g];
+      if (o == rank) {
+        for (int32_t d = 0; d < world; ++d)
+          if (d != rank && (holders[b] >> d & 1)) ++P.send_off[d + 1];
+      } else if (holders[b] >> rank & 1) {
+        ++P.recv_off[o + 1];
+      }
+    }
+  for (int32_t r = 0; r < world; ++r) {
+    P.send_off[r + 1] += P.send_off[r];
+    P.recv_off[r + 1] += P.recv_off[r];
+  }
+  P.send_count = P.send_off[world];
+  P.recv_count = P.recv_off[world];
+  P.send_obs_local.assign(P.send_count, -1);
+  P.gmap.assign(P.n_boundary_copies, -1);
   {
-    // input index -> local observation index
-    std::vector<int64_t> local_index_of_obs(l, -1);
-    for (size_t q = 0; q < P.local_obs.size(); ++q) local_index_of_obs[P.local_obs[q]] = (int64_t)q;
-    int64_t s = 0;
-    for (int64_t g = 0; g < P.n_boundary_copies; ++g)
-      if (g_owner[g] == rank) P.send_obs_local[s++] = local_index_of_obs[g_obs[g]];
+    std::vector<int64_t> sfill(P.send_off.begin(), P.send_off.end() - 1);
+    std::vector<int64_t> rfill(P.recv_off.begin(), P.recv_off.end() - 1);
+    for (int32_t b = 0; b < P.n_boundary_points; ++b)
+      for (int64_t g = P.gb_off[b]; g < P.gb_off[b + 1]; ++g) {
+        const int32_t o = g_owner[g];
+        if (o == rank) {
+          const int64_t q = local_index_of_obs[g_obs[g]];
+          P.gmap[g] = -2 - q;
+          for (int32_t d = 0; d < world; ++d)
+            if (d != rank && (holders[b] >> d & 1)) P.send_obs_local[sfill[d]++] = q;
+        } else if (holders[b] >> rank & 1) {
+          P.gmap[g] = rfill[o]++;
+        }
+      }
   }
   // comm_floats of the reference (admm_solver.cpp:74-101): sum_i 3 d_i (d_i - 1)
   std::vector<int64_t> d(n, 0);
@@ -201,7 +227,7 @@ void dbag_shard_plan_get_info(const dbag_shard_plan* s, dbag_shard_info* info) {
   info->boundary_points = p.n_boundary_points;
   info->boundary_copies = p.n_boundary_copies;
   info->send_count = p.send_count;
-  info->max_send = p.max_send;
+  info->recv_count = p.recv_count;
   info->comm_floats = p.comm_floats;
 }
 
@@ -220,6 +246,13 @@ int dbag_shard_plan_arrays(const dbag_shard_plan* s, int32_t* cam_lo, int64_t* l
   cp(gb_off, p.gb_off);
   cp(gmap, p.gmap);
   cp(send_obs_local, p.send_obs_local);
+  return DBAG_OK;
+}
+
+int dbag_shard_plan_exchange(const dbag_shard_plan* s, int64_t* send_off, int64_t* recv_off) {
+  const auto& p = s->p;
+  if (send_off) std::copy(p.send_off.begin(), p.send_off.end(), send_off);
+  if (recv_off) std::copy(p.recv_off.begin(), p.recv_off.end(), recv_off);
   return DBAG_OK;
 }
 

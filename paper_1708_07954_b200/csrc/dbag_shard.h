@@ -21,9 +21,16 @@ struct ShardPlan {
   int32_t n_boundary_points = 0;
   int64_t n_boundary_copies = 0;
   std::vector<int64_t> gb_off;          // [n_boundary_points+1] global boundary copy ranges
-  std::vector<int64_t> gmap;            // global boundary copy -> all-gather recv slot
-  std::vector<int64_t> send_obs_local;  // this rank's boundary copies (global order) -> local obs
-  int64_t send_count = 0, max_send = 1;
+  // Per-peer exchange (one ncclSend/ncclRecv pair per peer in one group): a
+  // boundary copy travels only to the OTHER ranks that hold its point.
+  // gmap[g] for every global boundary copy g: >= 0 recv slot (a peer's copy of
+  // a point this rank holds); -2 - q for this rank's own copy (local obs q);
+  // -1 when this rank does not hold the point.
+  std::vector<int64_t> gmap;
+  std::vector<int64_t> send_off;        // [world+1] send slots per destination peer
+  std::vector<int64_t> send_obs_local;  // [send_count] local obs of each send slot
+  std::vector<int64_t> recv_off;        // [world+1] recv slots per source peer
+  int64_t send_count = 0, recv_count = 0;
   int64_t comm_floats = 0;
   int64_t total_obs = 0;
   int32_t total_points = 0, total_cameras = 0;

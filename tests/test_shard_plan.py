@@ -54,12 +54,37 @@ def test_shard_plan_properties(world):
     d = np.bincount(p.obs_pt[np.isin(p.obs_pt, boundary)], minlength=p.num_points)[boundary]
     assert info["boundary_copies"] == d.sum()
     assert np.array_equal(np.diff(plans[0]["gb_off"]), d)
-    # gmap: a bijection onto the filled slots of the rank-major recv buffer
-    gm = plans[0]["gmap"]
-    assert len(np.unique(gm)) == len(gm)
-    assert sum(pl["info"]["send_count"] for pl in plans) == info["boundary_copies"]
+    # per-peer exchange: a copy of a boundary point travels from its owner to
+    # every OTHER rank holding the point, in global copy order
+    g_obs = np.lexsort((p.obs_cam, p.obs_pt))
+    g_obs = g_obs[np.isin(p.obs_pt[g_obs], boundary)]
+    g_owner = rank_of_cam[p.obs_cam[g_obs]]
+    g_pt = p.obs_pt[g_obs]
+    holds = np.zeros((world, p.num_points), bool)
+    holds[rank_of_cam[p.obs_cam], p.obs_pt] = True
     for r, pl in enumerate(plans):
-        assert np.array_equal(pl["gmap"], gm) and pl["info"]["max_send"] == info["max_send"]
+        gm, so, ro = pl["gmap"], pl["send_off"], pl["recv_off"]
+        local_of_obs = np.full(p.num_observations, -1)
+        local_of_obs[pl["local_obs"]] = np.arange(len(pl["local_obs"]))
+        mine = g_owner == r
+        held = holds[r, g_pt]
+        assert np.all(gm[mine] == -2 - local_of_obs[g_obs[mine]])
+        assert np.all(gm[~held] == -1)
+        peer = held & ~mine
+        # recv slots: from source s, s's copies of the points r holds, in order
+        for src in range(world):
+            sel = peer & (g_owner == src)
+            assert np.array_equal(gm[sel], np.arange(ro[src], ro[src + 1]))
+        assert ro[r + 1] == ro[r] and pl["info"]["recv_count"] == ro[-1]
+        # send slots to dest d: the same copies d expects from r
+        for dst in range(world):
+            sel = mine & holds[dst, g_pt] & (dst != r)
+            assert np.array_equal(pl["send_obs_local"][so[dst]:so[dst + 1]],
+                                  local_of_obs[g_obs[sel]])
+            assert so[dst + 1] - so[dst] == (plans[dst]["recv_off"][r + 1] -
+                                             plans[dst]["recv_off"][r])
+    for r, pl in enumerate(plans):
+        assert np.array_equal(pl["gb_off"], plans[0]["gb_off"])
         bpl = pl["bp_of_local"]
         glob = pl["local_points"]
         assert np.all((bpl >= 0) == np.isin(glob, boundary))
@@ -79,8 +104,9 @@ def _free_port():
 
 def _rank_main(rank, world, port, q):
     """One gloo rank: pack this rank's boundary copies (from the oracle's
-    post-local-update state), all-gather, recompute each boundary point's
-    consensus from the gathered copies in the plan's global order."""
+    post-local-update state) per peer, exchange them with one send/recv pair
+    per peer, recompute each boundary point's consensus from its copies (own
+    and received) in the plan's global order."""
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path[:0] = [root, os.path.join(root, "oracle")]
@@ -102,23 +128,43 @@ def _rank_main(rank, world, port, q):
     blk_of_obs[obs_of_block] = np.arange(len(obs_of_block))
     plan = admm.shard_plan(p, rank, world)
     info = plan["info"]
-    send = np.zeros((info["max_send"], 6))
+    so, ro = plan["send_off"], plan["recv_off"]
+    send = np.zeros((info["send_count"], 6))
     for slot, qi in enumerate(plan["send_obs_local"]):
         b = blk_of_obs[plan["local_obs"][qi]]
         send[slot, :3], send[slot, 3:] = lp[b], r[b]
-    gathered = [torch.zeros(info["max_send"] * 6, dtype=torch.float64) for _ in range(world)]
-    dist.all_gather(gathered, torch.from_numpy(send.reshape(-1)))
-    recv = torch.cat(gathered).numpy().reshape(-1, 6)
+    recv = np.zeros((info["recv_count"], 6))
+    reqs = []  # one send/recv pair per peer, as the NCCL group does
+    for q_ in range(world):
+        if q_ == rank:
+            continue
+        if so[q_ + 1] > so[q_]:
+            reqs.append(dist.isend(torch.from_numpy(send[so[q_]:so[q_ + 1]].copy()), q_))
+        if ro[q_ + 1] > ro[q_]:
+            buf = torch.zeros((ro[q_ + 1] - ro[q_], 6), dtype=torch.float64)
+            reqs.append((dist.irecv(buf, q_), q_, buf))
+    for rq in reqs:
+        if isinstance(rq, tuple):
+            rq[0].wait()
+            recv[ro[rq[1]]:ro[rq[1] + 1]] = rq[2].numpy()
+        else:
+            rq.wait()
+
+    def copy_of(slot):
+        if slot >= 0:
+            return recv[slot]
+        b = blk_of_obs[plan["local_obs"][-2 - slot]]
+        return np.concatenate([lp[b], r[b]])
     inv_rho = 1.0 / 1.3
     out = {}
     for i_loc, bp in enumerate(plan["bp_of_local"]):
         if bp < 0:
             continue
         g0, g1 = plan["gb_off"][bp], plan["gb_off"][bp + 1]
-        anc = recv[plan["gmap"][g0], :3].copy()
+        anc = copy_of(plan["gmap"][g0])[:3].copy()
         acc = [0.0, 0.0, 0.0]
         for g in range(g0, g1):
-            c = recv[plan["gmap"][g]]
+            c = copy_of(plan["gmap"][g])
             for k in range(3):
                 acc[k] += (c[k] - anc[k]) + inv_rho * c[3 + k]
         out[int(plan["local_points"][i_loc])] = [anc[k] + acc[k] / float(g1 - g0) for k in range(3)]
@@ -129,11 +175,12 @@ def _rank_main(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_gloo_two_rank_boundary_consensus_bit_exact():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_boundary_consensus_bit_exact(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=300) for _ in procs]
