@@ -57,6 +57,15 @@ Vec3 mat_vec(const Mat3& a, const Vec3& x) {
 // exact-numerics mode evaluates the same algorithm, so oracle and device agree
 // bit for bit; the reference's std::sin/std::cos (geometry.cpp:9-49) are
 // glibc's, whose last-ulp behaviour is unpinned like Eigen's.
+// tests/native/sincos_vs_glibc.cpp measures the distance (<= 1 ulp over 1e8
+// arguments). Built with -DORC_GLIBC_SINCOS (tests/test_glibc_sincos.py) the
+// oracle calls glibc instead: the reference's own geometry path.
+#ifdef ORC_GLIBC_SINCOS
+void det_sincos(double x, double* sn, double* cs) {
+  *sn = std::sin(x);
+  *cs = std::cos(x);
+}
+#else
 void det_sincos(double x, double* sn, double* cs) {
   constexpr double kH1 = 1.5707963267341256, kH2 = 6.077100506303966e-11,
                    kH3 = 2.0222662487959506e-21, kTwoOverPi = 0.6366197723675814;
@@ -90,6 +99,7 @@ void det_sincos(double x, double* sn, double* cs) {
     default: *sn = -c; *cs = s; break;
   }
 }
+#endif
 
 namespace {
 // proj/src/geometry.cpp:9-49

@@ -590,3 +590,29 @@ def test_local_block_error_leaves_consensus_and_duals(O, P, loss):
     assert f"local block {b}:" in str(oe.value) and f"local block {b}:" in str(ge.value)
     assert_state_identical(osol, g)
     g.close()
+
+
+def test_gpu_exact_against_glibc_geometry_oracle(O, P, tmp_path):
+    """the GPU's EXACT mode (det_sincos) against an oracle
+    built with glibc's sin/cos, the reference's own geometry path
+    (geometry.cpp:9-28): round 1 agrees to ~1e-12 on the objective and to a
+    few ulps on the residual maxima (tests/test_glibc_sincos.py pins the same
+    numbers on the CPU)."""
+    import os
+    from test_glibc_sincos import build_glibc_oracle, rel
+    lib = build_glibc_oracle(tmp_path)
+    arrays, init, scene = config_arrays(P, 1, 0)
+    O._lib = None
+    O._LIB_PATH = lib
+    try:
+        _, osol, g = pair(O, P, arrays, init, loss=0, max_iters=3)
+        ot = osol.run(scene.ground_truth.cam_pose, scene.ground_truth.points)
+    finally:
+        O._lib = None
+        O._LIB_PATH = os.path.join(os.path.dirname(O.__file__), "liboracle.so")
+    gt = g.run(scene.ground_truth)
+    r1 = {k: rel(ot[0][k], gt[0][k]) for k in ("mean_reproj_err", "max_primal_x", "max_primal_y")}
+    print("GPU EXACT vs glibc-geometry oracle, round 1:", r1)
+    assert r1["mean_reproj_err"] < 1e-11 and r1["max_primal_x"] < 1e-12
+    assert r1["max_primal_y"] < 1e-12
+    g.close()
