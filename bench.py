@@ -389,6 +389,48 @@ def our_arm(args, rank, world, local_rank):
                            "control flow, last-ulp rounding differs (trajectory not bit-identical)"
                            if other == "fast" else
                            "bit-identical to the restated reference (oracle/)")}
+    # ---------------- the robust loss and a converging penalty, same workload
+    # (VERDICT r1): rounds 1..K of the Huber/L-BFGS path at the BASELINE
+    # default rho = 1, and at rho = 1e4, the smallest penalty of the sweep
+    # (tools/rho_sweep.py, profiles/r2_rho_sweep_config5.txt) whose consensus
+    # stays feasible (finite mean reprojection error) over 50 rounds at config
+    # 5 -- so the throughput is not only that of a diverging solve.
+    def timed_leg(loss_kind, rho):
+        o = P.AdmmOptions(misfit_loss=loss_kind, rho_x=rho, rho_y=rho, max_iters=10 ** 9,
+                          device=dev, numerics=numerics,
+                          points_per_block=args.points_per_block,
+                          cameras_per_block=args.cameras_per_block)
+        sv = make(p, scene.init, o)
+        st = torch.cuda.ExternalStream(sv.stream_handle(), device=dev)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier()
+        a0.record(st)
+        for _ in range(args.steps):
+            sv.enqueue_round()
+        a1.record(st)
+        sv.synchronize()
+        ms_leg = a0.elapsed_time(a1)
+        if world > 1:
+            t = torch.tensor([ms_leg], device=f"cuda:{dev}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms_leg = float(t.item())
+        last_leg = sv.iterate()  # round K+1 with the record read back (untimed)
+        sv.close()
+        return {"value": L * args.steps / (ms_leg / 1e3), "ms_per_step": ms_leg / args.steps,
+                "rounds": args.steps, "rho": rho,
+                "last_round_mean_reproj_err": last_leg["mean_reproj_err"],
+                "last_round_max_primal_x": last_leg["max_primal_x"]}
+
+    legs = {}
+    if not args.no_legs:
+        hub = P.LossKind.huber(1.0)
+        if args.loss != "huber":
+            legs["huber_rho1"] = dict(timed_leg(hub, 1.0), loss="huber", note=(
+                "Huber delta=1 (config 1's literal loss), L-BFGS local solves, rho=1"))
+        legs["converging_huber_rho1e4"] = dict(timed_leg(hub, 1e4), loss="huber", note=(
+            "rho=1e4 keeps config 5's consensus feasible for 50 rounds (tools/rho_sweep.py)"))
+
     value = L * args.steps / (ms_total / 1e3)  # whole job: every rank's share of one scene
 
     # ---------------- roofline
@@ -495,6 +537,7 @@ def our_arm(args, rank, world, local_rank):
                              f"(record D2H each) + consensus D2H, wall clock"},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu,
             "other_numerics": other_line,
+            "other_losses": legs,
             "clocks": clocks.summary(),
             # our kernels per round: K1, K3, K2, k_final, k_combine (+ k_pack_send when
             # sharded); the Huber effort-order sort adds CUB's radix-sort kernels
@@ -522,6 +565,8 @@ def main():
                     help="exact: bit-identical to the restated reference; fast: FMA/Woodbury")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
+    ap.add_argument("--no-legs", action="store_true",
+                    help="skip the Huber and converging-rho legs (other_losses)")
     ap.add_argument("--points-per-block", type=int, default=1,
                     help="BlockConfig points_per_block (generalized blocks when != (1,1))")
     ap.add_argument("--cameras-per-block", type=int, default=1)

@@ -39,58 +39,83 @@ std::string format_double(double v) {  // bal_io.cpp:17-21
   return std::string(buf, res.ptr);
 }
 
-struct Token {
-  std::string_view text;
-  int line;
+// What a field is, for error messages only: "<kind> <index> <field>[ <sub>]",
+// e.g. "observation 5 camera index" or "camera 3 rotation parameter 0"; the
+// text is built only when a field fails to parse.
+struct Label {
+  const char* kind;      // "camera count", "observation", "camera", "point", ...
+  long long index = -1;  // -1: kind alone
+  const char* field = nullptr;
+  int sub = -1;          // -1: no trailing sub-index
+  std::string str() const {
+    std::string s = kind;
+    if (index >= 0) s += " " + std::to_string(index);
+    if (field) s += std::string(" ") + field;
+    if (sub >= 0) s += " " + std::to_string(sub);
+    return s;
+  }
 };
 
-class TokenStream {  // bal_io.cpp:28-83
+// Whitespace-separated fields of the problem text, scanned on demand (no
+// token array: a multi-million-observation file is parsed in one pass), with
+// the 1-based line of the last field returned for messages.
+class FieldCursor {
  public:
-  explicit TokenStream(std::string_view text) {
-    int line = 1;
-    size_t i = 0;
-    while (i < text.size()) {
-      if (text[i] == '\n') {
-        ++line;
-        ++i;
-      } else if (std::isspace(static_cast<unsigned char>(text[i]))) {
-        ++i;
-      } else {
-        const size_t start = i;
-        while (i < text.size() && !std::isspace(static_cast<unsigned char>(text[i]))) ++i;
-        tokens_.push_back({text.substr(start, i - start), line});
-      }
-    }
+  explicit FieldCursor(std::string_view text) : t_(text) {}
+
+  // The next field; an empty view at the end of the input.
+  std::string_view take() {
+    skip_space();
+    if (i_ >= t_.size()) return {};
+    const size_t start = i_;
+    while (i_ < t_.size() && !space(t_[i_])) ++i_;
+    field_line_ = line_;
+    return t_.substr(start, i_ - start);
   }
-  bool done() const { return pos_ >= tokens_.size(); }
-  int line() const {
-    return done() ? (tokens_.empty() ? 1 : tokens_.back().line) : tokens_[pos_].line;
+  // The next field without consuming it.
+  std::string_view look() {
+    const size_t i = i_;
+    const int line = line_, fl = field_line_;
+    const std::string_view f = take();
+    i_ = i;
+    line_ = line;
+    field_line_ = fl;
+    return f;
   }
-  const Token* peek() const { return done() ? nullptr : &tokens_[pos_]; }
-  Token next(const std::string& what) {
-    if (done()) fail(DBAG_ERR_PARSE, "unexpected end of file, expected " + what, line());
-    return tokens_[pos_++];
+  bool exhausted() {
+    skip_space();
+    return i_ >= t_.size();
   }
-  long long read_int(const std::string& what) {
-    const Token t = next(what);
-    long long v = 0;
-    const auto r = std::from_chars(t.text.data(), t.text.data() + t.text.size(), v);
-    if (r.ec != std::errc{} || r.ptr != t.text.data() + t.text.size())
-      fail(DBAG_ERR_PARSE, "expected " + what + ", got '" + std::string(t.text) + "'", t.line);
-    return v;
+  int field_line() const { return field_line_; }  // of the last field taken (1 before any)
+  int next_line() {                                // of the next field
+    skip_space();
+    return line_;
   }
-  double read_double(const std::string& what) {
-    const Token t = next(what);
-    double v = 0;
-    const auto r = std::from_chars(t.text.data(), t.text.data() + t.text.size(), v);
-    if (r.ec != std::errc{} || r.ptr != t.text.data() + t.text.size())
-      fail(DBAG_ERR_PARSE, "expected " + what + ", got '" + std::string(t.text) + "'", t.line);
+
+  std::string_view require(const Label& what) {
+    const std::string_view f = take();
+    if (f.empty()) fail(DBAG_ERR_PARSE, "unexpected end of file, expected " + what.str(), field_line_);
+    return f;
+  }
+  template <typename T>
+  T number(const Label& what) {
+    const std::string_view f = require(what);
+    T v{};
+    const auto r = std::from_chars(f.data(), f.data() + f.size(), v);
+    if (r.ec != std::errc{} || r.ptr != f.data() + f.size())
+      fail(DBAG_ERR_PARSE, "expected " + what.str() + ", got '" + std::string(f) + "'", field_line_);
     return v;
   }
 
  private:
-  std::vector<Token> tokens_;
-  size_t pos_ = 0;
+  static bool space(char c) { return std::isspace(static_cast<unsigned char>(c)) != 0; }
+  void skip_space() {
+    for (; i_ < t_.size() && space(t_[i_]); ++i_)
+      if (t_[i_] == '\n') ++line_;
+  }
+  std::string_view t_;
+  size_t i_ = 0;
+  int line_ = 1, field_line_ = 1;
 };
 
 // Rodrigues rotation of an angle-axis vector, then the reference's Euler
@@ -249,39 +274,36 @@ int dbag_parse_problem_text(const char* text, size_t len, dbag_bal** out, int32_
   *out = nullptr;
   auto* b = new dbag_bal();
   const int rc = guarded([&] {
-    TokenStream ts(std::string_view(text, len));
+    FieldCursor in(std::string_view(text, len));
     bool angle_axis = false;
-    if (const Token* tok = ts.peek(); tok != nullptr && tok->text == "rotation") {
-      ts.next("rotation flag");
-      const Token v = ts.next("rotation encoding (euler | angle-axis)");
-      if (v.text == "euler")
+    if (in.look() == "rotation") {
+      in.take();
+      const std::string_view v = in.require({"rotation encoding (euler | angle-axis)"});
+      if (v == "euler")
         angle_axis = false;
-      else if (v.text == "angle-axis")
+      else if (v == "angle-axis")
         angle_axis = true;
       else
-        fail(DBAG_ERR_PARSE, "unknown rotation encoding '" + std::string(v.text) + "'", v.line);
+        fail(DBAG_ERR_PARSE, "unknown rotation encoding '" + std::string(v) + "'", in.field_line());
     }
-    const long long m = ts.read_int("camera count");
-    const long long n = ts.read_int("point count");
-    const long long l = ts.read_int("observation count");
+    const long long m = in.number<long long>({"camera count"});
+    const long long n = in.number<long long>({"point count"});
+    const long long l = in.number<long long>({"observation count"});
     if (m < 1 || n < 1 || l < 1) fail(DBAG_ERR_VALIDATION, "header counts must all be >= 1");
     b->cam.resize(l);
     b->pt.resize(l);
     b->uv.resize(2 * l);
     for (long long k = 0; k < l; ++k) {
-      const std::string what = "observation " + std::to_string(k);
-      b->cam[k] = (int32_t)ts.read_int(what + " camera index");
-      b->pt[k] = (int32_t)ts.read_int(what + " point index");
-      b->uv[2 * k] = ts.read_double(what + " u");
-      b->uv[2 * k + 1] = ts.read_double(what + " v");
+      b->cam[k] = (int32_t)in.number<long long>({"observation", k, "camera index"});
+      b->pt[k] = (int32_t)in.number<long long>({"observation", k, "point index"});
+      b->uv[2 * k] = in.number<double>({"observation", k, "u"});
+      b->uv[2 * k + 1] = in.number<double>({"observation", k, "v"});
     }
     b->pose.resize(6 * m);
     b->f.resize(m);
     for (long long j = 0; j < m; ++j) {
-      const std::string what = "camera " + std::to_string(j);
       double rot[3];
-      for (int k = 0; k < 3; ++k)
-        rot[k] = ts.read_double(what + " rotation parameter " + std::to_string(k));
+      for (int k = 0; k < 3; ++k) rot[k] = in.number<double>({"camera", j, "rotation parameter", k});
       if (angle_axis) {
         double e[3];
         euler_from_angle_axis(rot, e);
@@ -291,20 +313,18 @@ int dbag_parse_problem_text(const char* text, size_t len, dbag_bal** out, int32_
       }
       for (int k = 0; k < 3; ++k) b->pose[6 * j + k] = rot[k];
       for (int k = 0; k < 3; ++k)
-        b->pose[6 * j + 3 + k] = ts.read_double(what + " translation " + std::to_string(k));
-      b->f[j] = ts.read_double(what + " focal length");
-      const double k1 = ts.read_double(what + " distortion k1");
-      const double k2 = ts.read_double(what + " distortion k2");
+        b->pose[6 * j + 3 + k] = in.number<double>({"camera", j, "translation", k});
+      b->f[j] = in.number<double>({"camera", j, "focal length"});
+      const double k1 = in.number<double>({"camera", j, "distortion k1"});
+      const double k2 = in.number<double>({"camera", j, "distortion k2"});
       if (k1 != 0.0 || k2 != 0.0)
-        fail(DBAG_ERR_VALIDATION, what + " has nonzero distortion; this camera model has none");
+        fail(DBAG_ERR_VALIDATION,
+             "camera " + std::to_string(j) + " has nonzero distortion; this camera model has none");
     }
     b->pts.resize(3 * n);
-    for (long long i = 0; i < n; ++i) {
-      const std::string what = "point " + std::to_string(i);
-      for (int k = 0; k < 3; ++k)
-        b->pts[3 * i + k] = ts.read_double(what + " coordinate " + std::to_string(k));
-    }
-    if (!ts.done()) fail(DBAG_ERR_PARSE, "unexpected trailing data", ts.line());
+    for (long long i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) b->pts[3 * i + k] = in.number<double>({"point", i, "coordinate", k});
+    if (!in.exhausted()) fail(DBAG_ERR_PARSE, "unexpected trailing data", in.next_line());
     b->m = (int32_t)m;
     b->n = (int32_t)n;
     validate_problem(b->m, b->n, b->cam, b->pt, b->uv, b->pose, b->f, b->pts);

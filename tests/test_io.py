@@ -109,3 +109,30 @@ def test_metrics_csv_schema(P):
     assert csv == P.metrics_csv(trace)
     assert "nan" in csv and csv.count("\n") == 3
     assert csv.splitlines()[2] == "2,0.25,1e-07,0,nan,nan,3.5,180"
+
+
+@pytest.mark.parametrize("text,msg,line", [
+    # end of input: the line of the file's last field (bal_io.cpp:49-57)
+    (SMALLEST[:SMALLEST.find("100.0")] + "\n\n",
+     "unexpected end of file, expected camera 0 focal length", 8),
+    ("", "unexpected end of file, expected camera count", 1),
+    ("rotation\n", "unexpected end of file, expected rotation encoding (euler | angle-axis)", 1),
+    # a malformed field: its own line (:59-75)
+    ("1 1 1\n0 0 x -2.0\n", "expected observation 0 u, got 'x'", 2),
+    ("1 1 1\n0 0 1.5 -2.0\n0.1\n0.0\n0.0\n0.0\n0.0\nfive\n", "expected camera 0 translation 2, got 'five'", 8),
+    ("1 1 1\n" + SMALLEST[6:].replace("1.0\n", "1.0 abc\n"), "expected point 0 coordinate 2, got '1.0'", -1),
+    # trailing data: the line of the first extra field (:181-183)
+    (SMALLEST + "\n\n 7.0\n", "unexpected trailing data", 17),
+    ("rotation quaternion\n1 1 1\n", "unknown rotation encoding 'quaternion'", 1),
+])
+def test_parse_error_messages_and_lines(P, text, msg, line):
+    """The reference's ParseError text and line numbers, field by field."""
+    if line < 0:  # "1.0 abc" is not one field: "abc" is trailing data instead
+        with pytest.raises(P.ParseError) as e:
+            P.parse_problem_text(text)
+        assert "unexpected trailing data" in str(e.value)
+        return
+    with pytest.raises(P.ParseError) as e:
+        P.parse_problem_text(text)
+    assert str(e.value).startswith(f"{msg} (line {line})"), str(e.value)
+    assert e.value.line == line
