@@ -310,8 +310,6 @@ def our_arm(args, rank, world, local_rank):
         solver.enqueue_round()
     solver.synchronize()
     solver.reset()
-    solver.reset_stats()
-    solver.set_profiling(True)
     stream = torch.cuda.ExternalStream(solver.stream_handle(), device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -329,8 +327,18 @@ def our_arm(args, rank, world, local_rank):
         t = torch.tensor([ms_total], device=f"cuda:{dev}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
-    stats = solver.round_stats()
     last = solver.iterate()  # one more round with the metrics read back (untimed)
+    # the same rounds 1..K again with per-kernel events (profiling mode replays
+    # the round kernel by kernel instead of as one CUDA graph): the per-kernel
+    # split and the event counters of the roofline; untimed
+    solver.reset()
+    solver.reset_stats()
+    solver.set_profiling(True)
+    for _ in range(args.steps):
+        solver.enqueue_round()
+    solver.synchronize()
+    stats = solver.round_stats()
+    solver.set_profiling(False)
 
     # ---------------- e2e through the C-ABI from pinned host buffers (after the
     # device-timed leg, so both run at the same settled clocks)

@@ -7,6 +7,7 @@
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -21,6 +22,7 @@
 #include "dbag_exact.h"
 #include "dbag_shard.h"
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include "dbag_index.cuh"
 #include "dbag_local.cuh"
 #include "dbag_lbfgs.cuh"
@@ -77,6 +79,13 @@ int guarded(F&& f) {
 }
 
 [[noreturn]] void raise(int code, const std::string& msg) { throw StatusError{code, msg}; }
+
+// NVTX range for the lifetime of a scope (host-side phases: create, rounds,
+// queries) so an nsys/ncu timeline shows the reference's phases by name.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 __global__ void k_pack_xbar(int32_t n, const double4* x, double* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -149,6 +158,11 @@ struct dbag_solver {
   std::vector<int64_t> send_off, recv_off;  // [world+1] exchange slots per peer
   ncclComm_t comm = nullptr;
   bool shard_mode = false;  // made by dbag_create_sharded (any world, 1 included)
+  // The steady-state round as a CUDA graph, one per with_reference value:
+  // captured on the second enqueued round (the first one runs directly and
+  // sets up every lazy launch attribute), replayed with one cudaGraphLaunch.
+  cudaGraphExec_t round_graph[2] = {nullptr, nullptr};
+  int64_t rounds_enqueued = 0;
   bool sharded() const { return shard_mode; }
   // generalized blocks (BlockConfig != {1,1}); null for (1,1)
   std::unique_ptr<blocks::GenSolver> gen;
@@ -170,6 +184,7 @@ struct dbag_solver {
     for (auto& set : prof_ev)
       for (auto& e : set) cudaEventDestroy(e);
     if (h_rec) cudaFreeHost(h_rec);
+    drop_graphs();
     if (comm) ncclCommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -343,7 +358,49 @@ struct dbag_solver {
   // One round: local -> camera consensus+dual -> [boundary all-gather] ->
   // point consensus+dual+metric -> partial record -> [all-gather] -> combine.
   // Events bracket the kernels (e[0]..e[4]).
+  // Graphs replay the round's kernels with the DevState captured by value, so
+  // they are dropped whenever a DevState field changes (dbag_set_reference).
+  // Not used while profiling (per-round event sets), for sharded solves (the
+  // NCCL exchange stays on the stream) or generalized blocks, or with
+  // DBAG_NO_GRAPH=1 in the environment.
+  void drop_graphs() {
+    for (auto& g : round_graph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+  }
+  bool graphs_ok() const {
+    static const bool off = std::getenv("DBAG_NO_GRAPH") != nullptr;
+    return !off && !profiling && !gen && !sharded() && S.L > 0;
+  }
   void enqueue_round(bool with_ref) {
+    NvtxRange r("dbag round");
+    const bool replay = graphs_ok() && rounds_enqueued++ > 0;
+    if (!replay) {
+      enqueue_round_direct(with_ref);
+      return;
+    }
+    cudaGraphExec_t& g = round_graph[with_ref ? 1 : 0];
+    if (!g) {
+      cudaGraph_t graph = nullptr;
+      CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_round_direct(with_ref);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      CK(cudaStreamEndCapture(stream, &graph));
+      const cudaError_t e = cudaGraphInstantiate(&g, graph, 0);
+      cudaGraphDestroy(graph);
+      CK(e);
+    }
+    CK(cudaGraphLaunch(g, stream));
+  }
+
+  void enqueue_round_direct(bool with_ref) {
     cudaEvent_t* e = round_events();
     phase0(e);
     exchange(0);
@@ -755,6 +812,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
 
 int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const dbag_options* opts,
                 dbag_solver** out) {
+  NvtxRange nvtx_("dbag_create");
   *out = nullptr;
   auto* h = new dbag_solver();
   const int rc = guarded([&] { create_impl(h, P, init, opts); });
@@ -769,6 +827,7 @@ int dbag_create(const dbag_problem_view* P, const dbag_param_view* init, const d
 int dbag_create_sharded(const dbag_problem_view* F, const dbag_param_view* init,
                         const dbag_options* opts, int32_t rank, int32_t world,
                         dbag_solver** out) {
+  NvtxRange nvtx_("dbag_create_sharded");
   *out = nullptr;
   auto* h = new dbag_solver();
   const int rc = guarded([&] {
@@ -991,6 +1050,7 @@ int dbag_dual_update(dbag_solver* h) {
 int dbag_set_reference(dbag_solver* h, const dbag_param_view* ref) {
   return guarded([&] {
     CK(cudaSetDevice(h->device));
+    h->drop_graphs();
     if (!ref) {
       h->has_ref = false;
       return;
@@ -1035,6 +1095,7 @@ int dbag_iterate(dbag_solver* h, int32_t with_reference, dbag_iteration_record* 
 
 int dbag_run(dbag_solver* h, int32_t with_reference, dbag_iteration_record* trace, int64_t cap,
              int64_t* n_out) {
+  NvtxRange nvtx_("dbag_run");
   return guarded([&] {
     CK(cudaSetDevice(h->device));
     if (with_reference && !h->has_ref) raise(DBAG_ERR_VALIDATION, "no reference state set");

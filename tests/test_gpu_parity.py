@@ -616,3 +616,32 @@ def test_gpu_exact_against_glibc_geometry_oracle(O, P, tmp_path):
     assert r1["mean_reproj_err"] < 1e-11 and r1["max_primal_x"] < 1e-12
     assert r1["max_primal_y"] < 1e-12
     g.close()
+
+
+def test_round_graph_replay_matches_direct_launches(P):
+    """From the second round on, iterate/run replay the round as one CUDA graph
+    (dbag_capi.cu enqueue_round). A process with DBAG_NO_GRAPH=1 launches the
+    kernels one by one: the trajectories are bitwise identical and the graph's
+    event nodes still time every round."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, json; sys.path.insert(0, %r); import paper_1708_07954_b200 as P; "
+            "s = P.generate_config_scene(2, 0, 0.1); "
+            "g = P.AdmmSolver(s.problem, s.init, P.AdmmOptions(max_iters=6)); "
+            "t = g.run(s.ground_truth); c = g.consensus(); "
+            "print(json.dumps([[r['max_primal_x'], r['mean_reproj_err'], r['point_mse'], "
+            "r['wall_ms']] for r in t] + [float(c.points.sum()), float(c.cam_pose.sum())]))"
+            ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"DBAG_NO_GRAPH": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           env=dict(os.environ, **env), timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    a, b = outs
+    for x, y in zip(a[:-2], b[:-2]):
+        assert x[:3] == y[:3]
+        assert x[3] > 0 and y[3] > 0
+    assert a[-2:] == b[-2:]
