@@ -312,9 +312,9 @@ struct dbag_solver {
   // Phase 0: local solve, camera consensus+dual, pack boundary copies.
   void phase0(cudaEvent_t* e) {
     reset_err();
-    CK(cudaEventRecord(e[0], stream));
+    mark(e[0]);
     launch_local(0, num_blocks());
-    CK(cudaEventRecord(e[1], stream));
+    mark(e[1]);
     S.gate = S.err_block;
     launch_camera(kModeConsensus | kModeDual);
     S.gate = nullptr;
@@ -322,14 +322,14 @@ struct dbag_solver {
       k_pack_send<<<grid_for(S.send_count, 256), 256, 0, stream>>>(S);
       CK_LAUNCH();
     }
-    CK(cudaEventRecord(e[2], stream));
+    mark(e[2]);
   }
   // Phase 1: point consensus+dual+metric, MSE, this rank's partial record.
   void phase1(cudaEvent_t* e, bool with_ref) {
     S.gate = S.err_block;
     launch_point(kModeConsensus | kModeDual, true);
     S.gate = nullptr;
-    CK(cudaEventRecord(e[3], stream));
+    mark(e[3]);
     if (with_ref) {
       k_mse<<<n_mse_parts, 256, 0, stream>>>(S);
       CK_LAUNCH();
@@ -342,7 +342,7 @@ struct dbag_solver {
     k_combine<<<1, 32, 0, stream>>>(S, sharded() ? S.metric_recv : S.metric_part, world, M_total,
                                     N_total);
     CK_LAUNCH();
-    CK(cudaEventRecord(e[4], stream));
+    mark(e[4]);
   }
 
   cudaEvent_t* round_events() {
@@ -363,6 +363,13 @@ struct dbag_solver {
   // Not used while profiling (per-round event sets), for sharded solves (the
   // NCCL exchange stays on the stream) or generalized blocks, or with
   // DBAG_NO_GRAPH=1 in the environment.
+  // Events inside a captured graph cannot be timed: during capture the
+  // per-kernel marks are skipped, and a replayed round is bracketed by ev[0]
+  // and ev[3] on the stream (its kernel split is only in profiling mode).
+  bool capturing = false, last_graphed = false;
+  void mark(cudaEvent_t e) {
+    if (!capturing) CK(cudaEventRecord(e, stream));
+  }
   void drop_graphs() {
     for (auto& g : round_graph)
       if (g) {
@@ -377,6 +384,7 @@ struct dbag_solver {
   void enqueue_round(bool with_ref) {
     NvtxRange r("dbag round");
     const bool replay = graphs_ok() && rounds_enqueued++ > 0;
+    last_graphed = replay;
     if (!replay) {
       enqueue_round_direct(with_ref);
       return;
@@ -385,19 +393,24 @@ struct dbag_solver {
     if (!g) {
       cudaGraph_t graph = nullptr;
       CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
       try {
         enqueue_round_direct(with_ref);
       } catch (...) {
+        capturing = false;
         cudaStreamEndCapture(stream, &graph);
         if (graph) cudaGraphDestroy(graph);
         throw;
       }
+      capturing = false;
       CK(cudaStreamEndCapture(stream, &graph));
       const cudaError_t e = cudaGraphInstantiate(&g, graph, 0);
       cudaGraphDestroy(graph);
       CK(e);
     }
+    CK(cudaEventRecord(ev[0], stream));
     CK(cudaGraphLaunch(g, stream));
+    CK(cudaEventRecord(ev[3], stream));
   }
 
   void enqueue_round_direct(bool with_ref) {
@@ -435,11 +448,16 @@ struct dbag_solver {
     std::memcpy(&eb, h_rec + kRecFields, sizeof(eb));
     float ms_round = 0.f, ms[4] = {0, 0, 0, 0};
     CK(cudaEventElapsedTime(&ms_round, ev[0], ev[3]));
-    for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]));
-    stats.ms_local = ms[0];
-    stats.ms_camera = ms[1];
-    stats.ms_point = ms[2];
-    stats.ms_final = ms[3];
+    if (last_graphed) {  // one graph launch: the kernel split is not observable
+      const double nan = std::numeric_limits<double>::quiet_NaN();
+      stats.ms_local = stats.ms_camera = stats.ms_point = stats.ms_final = nan;
+    } else {
+      for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]));
+      stats.ms_local = ms[0];
+      stats.ms_camera = ms[1];
+      stats.ms_point = ms[2];
+      stats.ms_final = ms[3];
+    }
     if (eb >= 0) {
       g_err_block = eb;
       raise(DBAG_ERR_GENERIC,
@@ -1512,6 +1530,8 @@ int dbag_get_round_stats(dbag_solver* h, dbag_round_stats* out) {
           CK(cudaEventElapsedTime(&ms, h->prof_ev[r][k], h->prof_ev[r][k + 1]));
           acc[k] += ms;
         }
+    } else if (h->last_graphed) {  // a replayed graph: no per-kernel split
+      for (int k = 0; k < 4; ++k) acc[k] = std::numeric_limits<double>::quiet_NaN();
     } else {
       for (int k = 0; k < 4; ++k) {
         float ms = 0.f;
