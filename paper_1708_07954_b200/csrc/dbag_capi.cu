@@ -274,8 +274,16 @@ struct dbag_solver {
     DevState So = S;
     So.order = nullptr;
     if (S.effort && begin == 0 && count == S.L && S.L > 0) {
-      CK(cub::DeviceRadixSort::SortPairs(order_tmp, order_tmp_bytes, S.effort, effort_sorted,
-                                         order_iota, order_buf, (int)S.L, 0, 16, stream));
+      // EXACT (pooled K1): heaviest first, so the pools drain evenly at the
+      // end; FAST (one thread per observation): ascending, so a warp holds
+      // solves of similar length. Stable either way (block order in ties).
+      if (exact())
+        CK(cub::DeviceRadixSort::SortPairsDescending(order_tmp, order_tmp_bytes, S.effort,
+                                                     effort_sorted, order_iota, order_buf,
+                                                     (int)S.L, 0, 16, stream));
+      else
+        CK(cub::DeviceRadixSort::SortPairs(order_tmp, order_tmp_bytes, S.effort, effort_sorted,
+                                           order_iota, order_buf, (int)S.L, 0, 16, stream));
       So.order = order_buf;
     }
     return So;
@@ -674,8 +682,12 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
       h->effort_sorted = dev_alloc<uint16_t>(pool, L);
       k_iota<<<grid_for(L, 256), 256, 0, st>>>(L, h->order_iota);
       CK_LAUNCH();
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, h->order_tmp_bytes, S.effort, h->effort_sorted,
+      size_t asc = 0, desc = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, asc, S.effort, h->effort_sorted,
                                          h->order_iota, h->order_buf, (int)L, 0, 16, st));
+      CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, desc, S.effort, h->effort_sorted,
+                                                   h->order_iota, h->order_buf, (int)L, 0, 16, st));
+      h->order_tmp_bytes = std::max(asc, desc);
       h->order_tmp = dev_alloc<char>(pool, h->order_tmp_bytes);
     }
 
