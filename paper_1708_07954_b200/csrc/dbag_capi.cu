@@ -677,6 +677,12 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
       // order it sorts into, and the sort's buffers
       S.effort = dev_alloc<uint16_t>(pool, L);
       CK(cudaMemsetAsync(S.effort, 0, sizeof(uint16_t) * (size_t)L, st));
+      if (opts->numerics == DBAG_NUMERICS_EXACT) {
+        const size_t nd = exact::huber_history_doubles();
+        if (nd == 0) raise(DBAG_ERR_CUDA, "pooled Huber K1: occupancy query failed");
+        S.hub_hist = dev_alloc<double>(pool, nd);
+        S.hub_hist_doubles = (int64_t)nd;
+      }
       h->order_buf = dev_alloc<int32_t>(pool, L);
       h->order_iota = dev_alloc<int32_t>(pool, L);
       h->effort_sorted = dev_alloc<uint16_t>(pool, L);

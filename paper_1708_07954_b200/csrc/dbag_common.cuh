@@ -103,6 +103,9 @@ struct DevState {
   // solve, and the processing order the next full launch uses (null: block order)
   uint16_t* effort;   // [L]
   const int32_t* order;  // [L] or null
+  // pooled Huber K1 (EXACT): L-BFGS histories, one record per resident slot
+  double* hub_hist;
+  int64_t hub_hist_doubles;
   // ---- multi-GPU shard (null/0 on a single-GPU solver) ----
   int32_t world, rank;
   int32_t* bp_of_local;   // [N] global boundary index of a local point, or -1

@@ -13,7 +13,9 @@ cudaError_t launch_local(const DevState& S, int64_t begin, int64_t count, cudaSt
 cudaError_t launch_camera(const DevState& S, int mode, cudaStream_t st);
 cudaError_t launch_point(const DevState& S, int mode, bool metric, int n_parts, cudaStream_t st);
 cudaError_t launch_camR_all(const DevState& S, cudaStream_t st);
-// the Huber K1 is the persistent lane-refill kernel (block order, no effort sort)
+// doubles of the pooled Huber K1's L-BFGS history scratch on the current
+// device (0 on error)
+size_t huber_history_doubles();
 // test hook: count n branch-free reciprocals that differ bitwise from IEEE 1/d
 cudaError_t selftest_rcp(int64_t n, unsigned long long seed, unsigned long long* bad_dev);
 }  // namespace exact
