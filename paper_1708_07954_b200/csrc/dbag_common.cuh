@@ -99,6 +99,7 @@ struct DevState {
   double* record;         // DevRecord
   double* metric_part;    // [kRecFields] this rank's partial record (raw sums)
   unsigned long long* work;  // K1 work counter (zeroed before each launch)
+  int32_t k1_batch;          // K1 claim batch (0: the kernel's default), set per launch
   // effort-ordered Huber K1: value evaluations of each observation's last local
   // solve, and the processing order the next full launch uses (null: block order)
   uint16_t* effort;   // [L]
@@ -155,80 +156,12 @@ __device__ __forceinline__ int64_t refill(const DevState& S, bool idle, int64_t 
   return idx < (unsigned long long)count ? (int64_t)idx : -1;
 }
 
-// refill() with a warp-local queue [q0, q1) of claimed indices: one global
-// atomic per kBatch observations instead of one per refill. Every index is
-// still taken exactly once; lanes take queue entries in lane order.
-struct WarpQueue {
-  unsigned long long q0 = 0, q1 = 0;  // warp-uniform
-  bool end = false;                   // a claim reached `count`
-};
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-// When a batch [base, base + n) is claimed, pull its observations' scattered
-// lines (point record, point consensus) and its camera-SoA rows into L2, so
-// the refills that consume the batch over the next iterations hit L2.
-__device__ __forceinline__ void prefetch_batch(const DevState& S, int64_t begin,
-                                               unsigned long long base, unsigned n,
-                                               int64_t count) {
-  const int lane = threadIdx.x & 31;
-  for (unsigned k = lane; k < n; k += 32) {
-    const unsigned long long e = base + k;
-    if (e < (unsigned long long)count) {
-      const int64_t b = begin + (int64_t)e;
-      prefetch_l2(S.prec + S.blk_pos[b]);
-      prefetch_l2(S.xbar + S.blk_pt[b]);
-    }
-  }
-  // 12 SoA rows of the batch: 8 B per observation, 128 B lines
-  const unsigned lines = (n + 15) / 16;
-  for (unsigned k = lane; k < 12 * lines; k += 32) {
-    const unsigned row = k / lines, ln = k % lines;
-    const unsigned long long e = base + 16ull * ln;
-    if (e < (unsigned long long)count) prefetch_l2(S.cam_soa + (int64_t)row * S.L + begin + (int64_t)e);
-  }
-}
-
-template <int kBatch, bool kPrefetch = false>
-__device__ __forceinline__ int64_t refill_batched(const DevState& S, bool idle, int64_t count,
-                                                  bool& exhausted, WarpQueue& q,
-                                                  int64_t begin = 0) {
-  const unsigned full = 0xffffffffu;
-  const unsigned m = __ballot_sync(full, idle && !exhausted);
-  if (m == 0) return -1;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(m) - 1;
-  const unsigned n = __popc(m);
-  const unsigned rank = __popc(m & ((1u << lane) - 1u));
-  const unsigned long long r = q.q1 - q.q0;
-  unsigned long long idx;
-  if (r >= n) {
-    idx = q.q0 + rank;
-    q.q0 += n;
-  } else {
-    const unsigned need = n - (unsigned)r;
-    const unsigned want = need > (unsigned)kBatch ? need : (unsigned)kBatch;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(S.work, (unsigned long long)want);
-    base = __shfl_sync(full, base, leader);
-    if (kPrefetch) prefetch_batch(S, begin, base + need, want - need, count);
-    idx = rank < r ? q.q0 + rank : base + (rank - r);
-    q.q0 = base + need;
-    q.q1 = base + want;
-    if (q.q1 >= (unsigned long long)count) {
-      q.end = true;
-      q.q1 = (unsigned long long)count;
-      if (q.q0 > q.q1) q.q0 = q.q1;
-    }
-  }
-  if (q.end && q.q0 >= q.q1) exhausted = true;
-  if (!(m & (1u << lane))) return -1;
-  return idx < (unsigned long long)count ? (int64_t)idx : -1;
-}
-
-// refill_batched with the warp's queue in shared memory (warp-uniform state
-// off the register file): every lane reads it, the leader writes it back.
+// refill() with a warp-local queue [q0, q1) of claimed indices, kept in shared
+// memory (warp-uniform state off the register file; every lane reads it, the
+// leader writes it back): one global atomic per batch of observations instead
+// of one per refill. Every index is still taken exactly once; lanes take queue
+// entries in lane order. The batch is kBatch, or S.k1_batch when smaller (a
+// small problem takes smaller batches, so the warps' last claims even out).
 struct WarpQueueS {
   unsigned long long q0, q1;
   unsigned end;
@@ -252,7 +185,9 @@ __device__ __forceinline__ int64_t refill_batched_s(const DevState& S, bool idle
     q0 += n;
   } else {
     const unsigned need = n - (unsigned)r;
-    const unsigned want = need > (unsigned)kBatch ? need : (unsigned)kBatch;
+    const unsigned bsz =
+        S.k1_batch > 0 && S.k1_batch < kBatch ? (unsigned)S.k1_batch : (unsigned)kBatch;
+    const unsigned want = need > bsz ? need : bsz;
     unsigned long long base = 0;
     if (lane == leader) base = atomicAdd(S.work, (unsigned long long)want);
     base = __shfl_sync(full, base, leader);
