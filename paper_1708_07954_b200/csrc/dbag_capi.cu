@@ -323,7 +323,9 @@ struct dbag_solver {
     mark(e[0]);
     launch_local(0, num_blocks());
     mark(e[1]);
+#ifndef DBAG_NO_GATE
     S.gate = S.err_block;
+#endif
     launch_camera(kModeConsensus | kModeDual);
     S.gate = nullptr;
     if (sharded() && S.send_count > 0) {
@@ -334,7 +336,9 @@ struct dbag_solver {
   }
   // Phase 1: point consensus+dual+metric, MSE, this rank's partial record.
   void phase1(cudaEvent_t* e, bool with_ref) {
+#ifndef DBAG_NO_GATE
     S.gate = S.err_block;
+#endif
     launch_point(kModeConsensus | kModeDual, true);
     S.gate = nullptr;
     mark(e[3]);

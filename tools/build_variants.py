@@ -23,6 +23,8 @@ VARIANTS = {
     "hub_q64": ["-DDBAG_HUB_Q=64", "-DDBAG_HUB_MINB=7"],
     # K2 exact: lanes per point
     "k2_g4": ["-DDBAG_K2E_G=4"],
+    # the consensus kernels without the round's error gate (A/B of its cost)
+    "nogate": ["-DDBAG_NO_GATE"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
     "fast_minb3": ["-DDBAG_K1_MINB=3"],
     # generalized blocks (dbag_blocks.cu)
@@ -37,7 +39,7 @@ def main(names):
     for n in names or VARIANTS:
         b.LIB = os.path.join(out, n + ".so")
         fl = VARIANTS[n]
-        fast = any("DBAG_FAST" in f or "DBAG_K1_" in f for f in fl)
+        fast = any("DBAG_FAST" in f or "DBAG_K1_" in f or "DBAG_NO_GATE" in f for f in fl)
         gen = any("DBAG_GEN" in f for f in fl)
         b.build(force=True, extra=fl, only=["dbag_blocks.cu" if gen else
                                             "dbag_capi.cu" if fast else "dbag_exact.cu"])
