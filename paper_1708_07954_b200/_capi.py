@@ -185,7 +185,11 @@ def load(build_if_missing=True):
         _b.build()
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and os.environ.get("DBAG_LIB"):
+            continue  # an older A/B build (tools/build_variants.py) may lack newer entry points
+        if fn is None:
+            raise ImportError(f"{LIB_PATH} does not export {name}")
         fn.restype = res
         fn.argtypes = args
     _lib = lib
