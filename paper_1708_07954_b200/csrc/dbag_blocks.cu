@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(kGenThreads, DBAG_GEN_MINB) k_local_blocks(
 // ---- camera consensus / dual over copies (admm_solver.cpp:333-355) --------
 constexpr int kGCamThreads = 128;
 __global__ void __launch_bounds__(kGCamThreads) k_gen_cameras(DevState S, GenState G, int mode) {
-  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
+  if (__syncthreads_or(threadIdx.x == 0 && S.gate && *S.gate >= 0)) return;  // local solve raised
   __shared__ double ybs[6];
   __shared__ double red[kGCamThreads / 32];
   const int j = blockIdx.x;
@@ -1046,7 +1046,7 @@ __global__ void __launch_bounds__(kGCamThreads) k_gen_cameras(DevState S, GenSta
 constexpr int kGPtThreads = 256;
 __global__ void __launch_bounds__(kGPtThreads) k_gen_points(DevState S, GenState G, int mode,
                                                             int metric) {
-  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
+  if (__syncthreads_or(threadIdx.x == 0 && S.gate && *S.gate >= 0)) return;  // local solve raised
   __shared__ double smem[(kGPtThreads / 32) * 2];
   const int64_t tix = (int64_t)blockIdx.x * kGPtThreads + threadIdx.x;
   double err_sum = 0.0, worst = 0.0, dual_res = 0.0, infeasible = 0.0;

@@ -244,10 +244,7 @@ struct dbag_solver {
       return;
     }
     if (exact()) {
-      CK(exact::launch_local(opts.loss == DBAG_LOSS_HUBER
-                                 ? effort_order(begin, count)
-                                 : S,
-                             begin, count, stream));
+      CK(exact::launch_local(effort_order(begin, count), begin, count, stream));
       return;
     }
     if (opts.loss == DBAG_LOSS_SQUARED_L2) {
@@ -323,9 +320,7 @@ struct dbag_solver {
     mark(e[0]);
     launch_local(0, num_blocks());
     mark(e[1]);
-#ifndef DBAG_NO_GATE
     S.gate = S.err_block;
-#endif
     launch_camera(kModeConsensus | kModeDual);
     S.gate = nullptr;
     if (sharded() && S.send_count > 0) {
@@ -336,9 +331,7 @@ struct dbag_solver {
   }
   // Phase 1: point consensus+dual+metric, MSE, this rank's partial record.
   void phase1(cudaEvent_t* e, bool with_ref) {
-#ifndef DBAG_NO_GATE
     S.gate = S.err_block;
-#endif
     launch_point(kModeConsensus | kModeDual, true);
     S.gate = nullptr;
     mark(e[3]);
@@ -578,6 +571,11 @@ void dbag_options_default(dbag_options* o) {
   o->numerics = DBAG_NUMERICS_EXACT;
 }
 
+#ifndef DBAG_EFFORT_MAX_L
+#define DBAG_EFFORT_MAX_L (8 << 20)
+#endif
+constexpr int64_t kEffortMaxL = DBAG_EFFORT_MAX_L;
+
 static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_param_view* init,
                         const dbag_options* opts) {
   {
@@ -676,12 +674,16 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     S.work = dev_alloc<unsigned long long>(pool, 1);
     S.effort = nullptr;
     S.order = nullptr;
-    if (opts->loss == DBAG_LOSS_HUBER) {
-      // effort-ordered Huber K1 (launch_local): per-observation effort, the
-      // order it sorts into, and the sort's buffers
+    // effort-ordered K1 (launch_local): per-observation effort of the last
+    // round, the order it sorts into (heaviest first for EXACT), and the sort's
+    // buffers. Huber always; EXACT squared L2 on scenes of at most kEffortMaxL
+    // observations, where the last claims' tail is a visible share of a round
+    // (config 2) and the per-round sort is cheap.
+    if (opts->loss == DBAG_LOSS_HUBER ||
+        (opts->numerics == DBAG_NUMERICS_EXACT && L <= kEffortMaxL)) {
       S.effort = dev_alloc<uint16_t>(pool, L);
       CK(cudaMemsetAsync(S.effort, 0, sizeof(uint16_t) * (size_t)L, st));
-      if (opts->numerics == DBAG_NUMERICS_EXACT) {
+      if (opts->numerics == DBAG_NUMERICS_EXACT && opts->loss == DBAG_LOSS_HUBER) {
         const size_t nd = exact::huber_history_doubles();
         if (nd == 0) raise(DBAG_ERR_CUDA, "pooled Huber K1: occupancy query failed");
         S.hub_hist = dev_alloc<double>(pool, nd);

@@ -35,7 +35,7 @@ __device__ __forceinline__ void write_camR(const DevState& S, int j, const doubl
 // K3: one CTA per camera segment [cam_off[j], cam_off[j+1]) of block order.
 template <int MODE>
 __global__ void __launch_bounds__(kCamThreads) k_camera(DevState S) {
-  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
+  if (__syncthreads_or(threadIdx.x == 0 && S.gate && *S.gate >= 0)) return;  // local solve raised
   __shared__ double smem[(kCamThreads / 32) * 6];
   __shared__ double ybar_s[6];
   const int j = blockIdx.x;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kCamThreads) k_camera(DevState S) {
 // the point-major record array.
 template <int MODE, bool kMetric>
 __global__ void __launch_bounds__(kPtThreads) k_point(DevState S) {
-  if (S.gate && *S.gate >= 0) return;  // the round's local solve raised
+  if (__syncthreads_or(threadIdx.x == 0 && S.gate && *S.gate >= 0)) return;  // local solve raised
   __shared__ double smem[(kPtThreads / 32) * 2];
   const int64_t t = (int64_t)blockIdx.x * kPtThreads + threadIdx.x;
   double err_sum = 0.0, worst = 0.0, dual_res = 0.0, infeasible = 0.0;

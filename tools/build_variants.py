@@ -17,14 +17,14 @@ VARIANTS = {
     "exact_t192": ["-DDBAG_K1E_THREADS=192"],
     "exact_batch32": ["-DDBAG_K1E_BATCH=32"],
     "exact_batch128": ["-DDBAG_K1E_BATCH=128"],
+    "exact_effort_off": ["-DDBAG_EFFORT_MAX_L=0"],
     # EXACT K1, Huber (dbag_exact.cu k_local_huber_pool): pool size / CTAs per SM
     "hub_q40": ["-DDBAG_HUB_Q=40", "-DDBAG_HUB_MINB=12"],
     "hub_q56": ["-DDBAG_HUB_Q=56", "-DDBAG_HUB_MINB=8"],
     "hub_q64": ["-DDBAG_HUB_Q=64", "-DDBAG_HUB_MINB=7"],
+    "k2_minb4": ["-DDBAG_K2E_MINB=4"],
     # K2 exact: lanes per point
     "k2_g4": ["-DDBAG_K2E_G=4"],
-    # the consensus kernels without the round's error gate (A/B of its cost)
-    "nogate": ["-DDBAG_NO_GATE"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
     "fast_minb3": ["-DDBAG_K1_MINB=3"],
     # generalized blocks (dbag_blocks.cu)
@@ -39,7 +39,7 @@ def main(names):
     for n in names or VARIANTS:
         b.LIB = os.path.join(out, n + ".so")
         fl = VARIANTS[n]
-        fast = any("DBAG_FAST" in f or "DBAG_K1_" in f or "DBAG_NO_GATE" in f for f in fl)
+        fast = any("DBAG_FAST" in f or "DBAG_K1_" in f or "DBAG_EFFORT" in f for f in fl)
         gen = any("DBAG_GEN" in f for f in fl)
         b.build(force=True, extra=fl, only=["dbag_blocks.cu" if gen else
                                             "dbag_capi.cu" if fast else "dbag_exact.cu"])
