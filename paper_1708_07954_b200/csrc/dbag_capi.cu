@@ -572,7 +572,7 @@ void dbag_options_default(dbag_options* o) {
 }
 
 #ifndef DBAG_EFFORT_MAX_L
-#define DBAG_EFFORT_MAX_L (8 << 20)
+#define DBAG_EFFORT_MAX_L (1 << 20)
 #endif
 constexpr int64_t kEffortMaxL = DBAG_EFFORT_MAX_L;
 
