@@ -112,6 +112,11 @@ class ParamState:
     def copy(self):
         return ParamState(self.cam_pose.copy(), self.cam_f.copy(), self.points.copy())
 
+    def as_f64(self):
+        """float64, C-contiguous views of the arrays (a copy only where needed);
+        the caller's object is not modified."""
+        return ParamState(_f64(self.cam_pose, (-1, 6)), _f64(self.cam_f), _f64(self.points, (-1, 3)))
+
     def _view(self):
         self.cam_pose = _f64(self.cam_pose, (-1, 6))
         self.cam_f = _f64(self.cam_f)
@@ -391,7 +396,7 @@ class AdmmSolver:
         self.problem = problem
         self.opts = opts or AdmmOptions()
         self._h = C.c_void_p()
-        init = init.copy()
+        init = init.as_f64()  # the C-ABI copies it to the device during create
         pv, iv, o = problem._view(), init._view(), self.opts._c()
         self.rank, self.world = rank, world
         if world == 1 and not sharded:
@@ -455,7 +460,7 @@ class AdmmSolver:
             return 0
         key = (id(reference.cam_pose), id(reference.points))
         if key != self._ref_key:
-            ref = reference.copy()
+            ref = reference.as_f64()
             v = ref._view()
             _check(self._lib.dbag_set_reference(self._h, C.byref(v)))
             self._ref_key = key
@@ -479,10 +484,17 @@ class AdmmSolver:
     def iteration(self):
         return self._lib.dbag_iteration(self._h)
 
-    def consensus(self) -> ParamState:
-        pose, f, pts = np.zeros((self.m, 6)), np.zeros(self.m), np.zeros((self.n, 3))
-        _check(self._lib.dbag_get_consensus(self._h, _dp(pose), _dp(f), _dp(pts)))
-        return ParamState(pose, f, pts)
+    def consensus(self, out: ParamState | None = None) -> ParamState:
+        """state().consensus; `out` (float64, C-contiguous, e.g. pinned host
+        buffers) is filled in place when given."""
+        if out is None:
+            out = ParamState(np.zeros((self.m, 6)), np.zeros(self.m), np.zeros((self.n, 3)))
+        for a in (out.cam_pose, out.cam_f, out.points):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError("consensus(out=...) needs float64 C-contiguous arrays")
+        _check(self._lib.dbag_get_consensus(self._h, _dp(out.cam_pose), _dp(out.cam_f),
+                                            _dp(out.points)))
+        return out
 
     def set_consensus(self, state: ParamState):
         pose, pts = _f64(state.cam_pose, (-1, 6)), _f64(state.points, (-1, 3))

@@ -7,6 +7,7 @@
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -120,11 +121,35 @@ namespace {
 
 inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// A handle's device buffers. Inside dbag_create they come from the device's
+// stream-ordered pool on the handle's stream (g_alloc_stream, set by
+// AllocScope): the pool keeps memory between handles, so creating a solver
+// after another was destroyed maps no new memory (cudaMalloc of ~6 GB at
+// config 5 took 4-140 ms). Freed with cudaFreeAsync on the same stream.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+thread_local bool g_alloc_async = false;
+struct AllocScope {
+  explicit AllocScope(cudaStream_t s) {
+    g_alloc_stream = s;
+    g_alloc_async = true;
+  }
+  ~AllocScope() {
+    g_alloc_stream = nullptr;
+    g_alloc_async = false;
+  }
+};
+
 template <typename T>
 T* dev_alloc(std::vector<void*>& pool, size_t count) {
   void* p = nullptr;
-  CK(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
-  pool.push_back(p);
+  const size_t bytes = sizeof(T) * (count ? count : 1);
+  if (g_alloc_async) {
+    CK(cudaMallocAsync(&p, bytes, g_alloc_stream));
+    pool.push_back(reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(p) | 1u));  // tag: async
+  } else {
+    CK(cudaMalloc(&p, bytes));
+    pool.push_back(p);
+  }
   return static_cast<T*>(p);
 }
 
@@ -178,7 +203,14 @@ struct dbag_solver {
   ~dbag_solver() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (void* p : pool) cudaFree(p);
+    for (void* p : pool) {
+      const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+      if (u & 1u)
+        cudaFreeAsync(reinterpret_cast<void*>(u & ~uintptr_t(1)), stream);
+      else
+        cudaFree(p);
+    }
+    if (stream) cudaStreamSynchronize(stream);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& set : prof_ev)
@@ -576,8 +608,24 @@ void dbag_options_default(dbag_options* o) {
 #endif
 constexpr int64_t kEffortMaxL = DBAG_EFFORT_MAX_L;
 
+// DBAG_CREATE_TIMING=1: host wall time of create's stages on stderr (the
+// stream is synchronized at each checkpoint, so it slows create a little).
+struct CreateClock {
+  bool on = std::getenv("DBAG_CREATE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "dbag_create %-28s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_param_view* init,
                         const dbag_options* opts) {
+  CreateClock clk;
   {
     const int M = P->num_cameras, N = P->num_points;
     const int64_t L = P->num_obs;
@@ -594,31 +642,58 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     }
     h->device = opts->device;
     CK(cudaSetDevice(h->device));
+    {
+      // create's temporaries come from the device's default stream-ordered
+      // pool; keep what it has mapped between creates (the default threshold
+      // 0 returns it at every synchronization, so each create re-mapped its
+      // ~2 GB of sort buffers at config 5)
+      cudaMemPool_t mp;
+      CK(cudaDeviceGetDefaultMemPool(&mp, h->device));
+      uint64_t keep = UINT64_MAX;
+      CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    AllocScope alloc_scope(h->stream);
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaMallocHost(&h->h_rec, sizeof(double) * (kRecFields + 2)));
     cudaStream_t st = h->stream;
+    clk.mark("context/stream/events", st);
     auto& pool = h->pool;
     IndexErrors* d_err = dev_alloc<IndexErrors>(pool, 1);
     CK(cudaMemsetAsync(d_err, 0xff, sizeof(IndexErrors), st));
     IndexErrors herr;
     if (P->points && N > 0) {
       double* d_np = nullptr;
-      CK(cudaMalloc(&d_np, sizeof(double) * 3 * N));
+      CK(cudaMallocAsync(&d_np, sizeof(double) * 3 * N, st));
       CK(cudaMemcpyAsync(d_np, P->points, sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
       k_check_points<<<grid_for(N, 256), 256, 0, st>>>(N, d_np, d_err);
       CK_LAUNCH();
       CK(cudaMemcpyAsync(&herr, d_err, sizeof(herr), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      cudaFree(d_np);
+      CK(cudaFreeAsync(d_np, st));
       if (herr.bad_point != ~0ull)
         raise(DBAG_ERR_VALIDATION,
               "point " + std::to_string(herr.bad_point) + " has non-finite coordinates");
     }
     // observations to the device (input order)
-    int32_t* d_cam = dev_alloc<int32_t>(pool, L);
-    int32_t* d_pt = dev_alloc<int32_t>(pool, L);
-    double* d_uv = dev_alloc<double>(pool, 2 * L);
+    // input-order observations: stream-ordered temporaries (create's only
+    // large frees; cudaFree would synchronize the device for each)
+    int32_t* d_cam = nullptr;
+    int32_t* d_pt = nullptr;
+    double* d_uv = nullptr;
+    CK(cudaMallocAsync(&d_cam, sizeof(int32_t) * std::max<int64_t>(L, 1), st));
+    CK(cudaMallocAsync(&d_pt, sizeof(int32_t) * std::max<int64_t>(L, 1), st));
+    CK(cudaMallocAsync(&d_uv, sizeof(double) * 2 * std::max<int64_t>(L, 1), st));
+    struct TmpInputs {  // released on every exit path, errors included
+      int32_t *&c, *&p;
+      double*& u;
+      cudaStream_t s;
+      ~TmpInputs() {
+        if (c) cudaFreeAsync(c, s);
+        if (p) cudaFreeAsync(p, s);
+        if (u) cudaFreeAsync(u, s);
+      }
+    } tmp_inputs{d_cam, d_pt, d_uv, st};
     if (L) {
       CK(cudaMemcpyAsync(d_cam, P->obs_cam, sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(d_pt, P->obs_pt, sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
@@ -643,6 +718,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
       raise(DBAG_ERR_INDEX_OUT_OF_RANGE,
             "point index " + std::to_string(p) + " outside [0, " + std::to_string(N) + ")");
     }
+    clk.mark("H2D + input checks", st);
     // ---- persistent device state
     DevState& S = h->S;
     S.L = L;
@@ -703,6 +779,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
       h->order_tmp = dev_alloc<char>(pool, h->order_tmp_bytes);
     }
 
+    clk.mark("persistent allocations", st);
     S.world = 1;
     S.rank = 0;
     CK(cudaMemsetAsync(S.counters, 0, sizeof(unsigned long long) * 8 * kCounterStripes, st));
@@ -732,13 +809,13 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
       uint32_t* ptk_s = nullptr;
       int32_t* iota = nullptr;
       int32_t* pm_blk = nullptr;
-      CK(cudaMalloc(&keys, 8 * L));
-      CK(cudaMalloc(&keys_s, 8 * L));
-      CK(cudaMalloc(&vals, 4 * L));
-      CK(cudaMalloc(&ptk, 4 * std::max<int64_t>(L, N)));
-      CK(cudaMalloc(&ptk_s, 4 * std::max<int64_t>(L, N)));
-      CK(cudaMalloc(&iota, 4 * std::max<int64_t>(L, N)));
-      CK(cudaMalloc(&pm_blk, 4 * std::max<int64_t>(L, N)));
+      CK(cudaMallocAsync(&keys, 8 * L, st));
+      CK(cudaMallocAsync(&keys_s, 8 * L, st));
+      CK(cudaMallocAsync(&vals, 4 * L, st));
+      CK(cudaMallocAsync(&ptk, 4 * std::max<int64_t>(L, N), st));
+      CK(cudaMallocAsync(&ptk_s, 4 * std::max<int64_t>(L, N), st));
+      CK(cudaMallocAsync(&iota, 4 * std::max<int64_t>(L, N), st));
+      CK(cudaMallocAsync(&pm_blk, 4 * std::max<int64_t>(L, N), st));
       k_make_keys<<<grid_for(L, 256), 256, 0, st>>>(L, d_cam, d_pt, keys, vals);
       CK_LAUNCH();
       int cam_bits = 1;
@@ -751,7 +828,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
                                                    std::max(N, 1), 0, 32, st));
       tmp_bytes = std::max(tmp_bytes, std::max(t2, t3));
       void* tmp = nullptr;
-      CK(cudaMalloc(&tmp, tmp_bytes));
+      CK(cudaMallocAsync(&tmp, tmp_bytes, st));
       CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, vals, S.blk_obs, (int)L, 0,
                                          32 + cam_bits, st));
       k_blocks_from_sorted<<<grid_for(L, 256), 256, 0, st>>>(L, M, keys_s, S, d_err, ptk, iota);
@@ -777,7 +854,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
       h->comm_floats = (int64_t)comm;
       for (void* p : {(void*)keys, (void*)keys_s, (void*)vals, (void*)ptk, (void*)ptk_s,
                       (void*)iota, (void*)pm_blk, tmp})
-        cudaFree(p);
+        CK(cudaFreeAsync(p, st));
       if (herr.dup_pos != ~0ull) {
         int32_t c, p;
         CK(cudaMemcpy(&c, S.blk_cam + herr.dup_pos, 4, cudaMemcpyDeviceToHost));
@@ -792,6 +869,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
         raise(DBAG_ERR_VALIDATION,
               "point " + std::to_string(herr.empty_pt) + " is observed by no camera");
     }
+    clk.mark("K0 sorts + index build", st);
     // ---- AdmmSolver::AdmmSolver (admm_solver.cpp:103-142)
     if (!(o.rho_x > 0.0) || !(o.rho_y > 0.0))
       raise(DBAG_ERR_VALIDATION, "penalty parameters must be positive");
@@ -808,7 +886,7 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     double* d_ipts = nullptr;
     double* d_if = nullptr;
     CK(cudaMalloc(&d_ipose, sizeof(double) * 6 * std::max(M, 1)));
-    CK(cudaMalloc(&d_if, sizeof(double) * std::max(M, 1)));
+    CK(cudaMallocAsync(&d_if, sizeof(double) * std::max(M, 1), st));
     CK(cudaMalloc(&d_ipts, sizeof(double) * 3 * std::max(N, 1)));
     CK(cudaMemcpyAsync(d_ipose, init->cam_pose, sizeof(double) * 6 * M, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(d_if, init_f, sizeof(double) * M, cudaMemcpyHostToDevice, st));
@@ -823,15 +901,12 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     h->init_pts = d_ipts;
     pool.push_back(d_ipose);
     pool.push_back(d_ipts);
-    cudaFree(d_if);
-    // input-order observation arrays are no longer needed
-    for (void* p : {(void*)d_cam, (void*)d_pt, (void*)d_uv}) {
-      cudaFree(p);
-      for (auto& q : pool)
-        if (q == p) q = nullptr;
-    }
+    CK(cudaFreeAsync(d_if, st));
+    // the input-order observation arrays are released by tmp_inputs
+    clk.mark("init state", st);
     // init must be feasible (admm_solver.cpp:116 -> problem.cpp:140-157)
     h->reproj_sum(1, true);
+    clk.mark("init feasibility", st);
     if (o.numerics != DBAG_NUMERICS_FAST && o.numerics != DBAG_NUMERICS_EXACT)
       raise(DBAG_ERR_VALIDATION, "numerics must be FAST (0) or EXACT (1)");
     if (o.points_per_block < 1 || o.cameras_per_block < 1)
