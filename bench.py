@@ -350,9 +350,12 @@ def our_arm(args, rank, world, local_rank):
                          pinned(np.zeros((p.num_points, 3))))
     t0 = time.perf_counter()
     s_e2e = make(hp, hinit, opts(args.steps))
+    t_c = time.perf_counter()
     trace = s_e2e.run()
+    t_r = time.perf_counter()
     s_e2e.consensus(out=final)
     t_e2e = time.perf_counter() - t0
+    e2e_stages = {"create_s": t_c - t0, "rounds_s": t_r - t_c, "consensus_d2h_s": t0 + t_e2e - t_r}
     if world > 1:
         t = torch.tensor([t_e2e], device=f"cuda:{dev}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -542,7 +545,8 @@ def our_arm(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, DESIGN.md §Inputs)",
             "config": config_block(args, p.num_cameras, p.num_points, L),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
+            "e2e": {"value": e2e_value, "unit": UNIT, "stages": e2e_stages,
+                    "h2d_bytes_per_step": h2d / args.steps,
                     "d2h_bytes_per_step": d2h / args.steps,
                     "scope": f"dbag_create (H2D + device index build) + {args.steps} rounds "
                              f"(record D2H each) + consensus D2H, wall clock"},

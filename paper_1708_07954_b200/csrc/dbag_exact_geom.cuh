@@ -176,9 +176,12 @@ __device__ __forceinline__ void ejac(const double v[9], const ETrig& t, const do
   ejac_inv(v, t, R, w, __drcp_rn(w[2]), f, A0, A1);
 }
 
+// sum of squares, sequential from 0.0 (oracle.cpp sqn). The first term is
+// taken as the start value: a square is never -0, and 0.0 + p == p bitwise
+// for every other p.
 __device__ __forceinline__ double sqn(const double* a, int n) {
-  double s = 0.0;
-  for (int i = 0; i < n; ++i) s += a[i] * a[i];
+  double s = a[0] * a[0];
+  for (int i = 1; i < n; ++i) s += a[i] * a[i];
   return s;
 }
 

@@ -13,6 +13,12 @@ from paper_1708_07954_b200 import build as b  # noqa: E402
 VARIANTS = {
     "cur": [],
     # EXACT K1, squared L2 (dbag_exact.cu k_local_gn_exact)
+    "exact_t352": ["-DDBAG_K1E_THREADS=352", "-DDBAG_K1E_MAXREG=176"],
+    "exact_zglobal": ["-DDBAG_K1E_ZGLOBAL"],
+    "exact_r255": ["-DDBAG_K1E_MINB=2"],
+    "exact_t160": ["-DDBAG_K1E_THREADS=160", "-DDBAG_K1E_MAXREG=192"],
+    "exact_t96m3": ["-DDBAG_K1E_THREADS=96", "-DDBAG_K1E_MAXREG=224"],
+    "exact_t256m1": ["-DDBAG_K1E_THREADS=256", "-DDBAG_K1E_MINB=1"],
     "exact_t96": ["-DDBAG_K1E_THREADS=96"],
     "exact_t192": ["-DDBAG_K1E_THREADS=192"],
     "exact_batch32": ["-DDBAG_K1E_BATCH=32"],
