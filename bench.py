@@ -328,6 +328,22 @@ def our_arm(args, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
     last = solver.iterate()  # one more round with the metrics read back (untimed)
+    # The reference's IterationRecord carries +inf when any consensus point
+    # projects at depth <= eps (admm_solver.cpp:437-460). The bench line must stay
+    # strict JSON, so a non-finite value becomes null, plus the first offending
+    # pair from the throwing variant (problem.cpp mean_reprojection_error).
+    last_round = {k: last[k] for k in ("iter", "mean_reproj_err", "max_primal_x",
+                                       "max_primal_y", "max_dual_x", "max_dual_y")}
+    if rank == 0 and not math.isfinite(last_round["mean_reproj_err"]):
+        last_round["mean_reproj_err"] = None
+        last_round["mean_reproj_err_note"] = "non-finite"
+        try:
+            if world == 1:
+                solver.mean_reprojection_error()
+        except P.admm.DepthBelowGuard as e:
+            last_round["mean_reproj_err_note"] = (
+                f"+inf per the reference's rule: consensus point {e.point_id} at depth "
+                f"{e.depth:.3g} <= eps in camera {e.cam_id} (first offender)")
     # the same rounds 1..K again with per-kernel events (profiling mode replays
     # the round kernel by kernel instead of as one CUDA graph): the per-kernel
     # split and the event counters of the roofline; untimed
@@ -339,6 +355,10 @@ def our_arm(args, rank, world, local_rank):
     solver.synchronize()
     stats = solver.round_stats()
     solver.set_profiling(False)
+    plan_info = solver.plan["info"] if world > 1 else None
+    # done with the resident solver: its device buffers go back to the
+    # stream-ordered pool, where the e2e handle's create finds them
+    solver.close()
 
     # ---------------- e2e through the C-ABI from pinned host buffers (after the
     # device-timed leg, so both run at the same settled clocks)
@@ -455,7 +475,7 @@ def our_arm(args, rank, world, local_rank):
     # per-rank work (a shard's kernels see its own observations/points/cameras)
     ncam, npt, Lr = p.num_cameras, p.num_points, L
     if world > 1:
-        inf_ = solver.plan["info"]
+        inf_ = plan_info
         ncam, npt, Lr = inf_["cam_end"] - inf_["cam_begin"], inf_["local_points"], inf_["local_obs"]
     for name, key in (("local", "ms_local"), ("camera", "ms_camera"), ("point", "ms_point")):
         ms = stats[key] / args.steps
@@ -520,23 +540,6 @@ def our_arm(args, rank, world, local_rank):
                          f"(local+consensus+dual), oracle/ restatement (reference needs "
                          f"Eigen3, absent)"}
 
-    # The reference's IterationRecord carries +inf when any consensus point
-    # projects at depth <= eps (admm_solver.cpp:437-460). The bench line must stay
-    # strict JSON, so a non-finite value becomes null, plus the first offending
-    # pair from the throwing variant (problem.cpp mean_reprojection_error).
-    last_round = {k: last[k] for k in ("iter", "mean_reproj_err", "max_primal_x",
-                                       "max_primal_y", "max_dual_x", "max_dual_y")}
-    if rank == 0 and not math.isfinite(last_round["mean_reproj_err"]):
-        last_round["mean_reproj_err"] = None
-        last_round["mean_reproj_err_note"] = "non-finite"
-        try:
-            if world == 1:
-                solver.mean_reprojection_error()
-        except P.admm.DepthBelowGuard as e:
-            last_round["mean_reproj_err_note"] = (
-                f"+inf per the reference's rule: consensus point {e.point_id} at depth "
-                f"{e.depth:.3g} <= eps in camera {e.cam_id} (first offender)")
-
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -562,7 +565,6 @@ def our_arm(args, rank, world, local_rank):
             "last_round": last_round,
         }
         print(json.dumps(_finite(line), allow_nan=False), flush=True)
-    solver.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0

@@ -13,12 +13,6 @@ from paper_1708_07954_b200 import build as b  # noqa: E402
 VARIANTS = {
     "cur": [],
     # EXACT K1, squared L2 (dbag_exact.cu k_local_gn_exact)
-    "exact_t352": ["-DDBAG_K1E_THREADS=352", "-DDBAG_K1E_MAXREG=176"],
-    "exact_zglobal": ["-DDBAG_K1E_ZGLOBAL"],
-    "exact_r255": ["-DDBAG_K1E_MINB=2"],
-    "exact_t160": ["-DDBAG_K1E_THREADS=160", "-DDBAG_K1E_MAXREG=192"],
-    "exact_t96m3": ["-DDBAG_K1E_THREADS=96", "-DDBAG_K1E_MAXREG=224"],
-    "exact_t256m1": ["-DDBAG_K1E_THREADS=256", "-DDBAG_K1E_MINB=1"],
     "exact_t96": ["-DDBAG_K1E_THREADS=96"],
     "exact_t192": ["-DDBAG_K1E_THREADS=192"],
     "exact_batch32": ["-DDBAG_K1E_BATCH=32"],
@@ -29,6 +23,10 @@ VARIANTS = {
     "hub_q56": ["-DDBAG_HUB_Q=56", "-DDBAG_HUB_MINB=8"],
     "hub_q64": ["-DDBAG_HUB_Q=64", "-DDBAG_HUB_MINB=7"],
     "k2_minb4": ["-DDBAG_K2E_MINB=4"],
+    # K3 exact: the streamed persistent kernel off / ring depth
+    "k3_percam": ["-DDBAG_K3_STREAM_MIN_OBS=2000000000"],
+    "k3_stream": ["-DDBAG_K3_STREAM_MIN_OBS=1024"],
+    "k3_stream_p7": ["-DDBAG_K3_STREAM_MIN_OBS=1024", "-DDBAG_K3S_PROD=7"],
     # K2 exact: lanes per point
     "k2_g4": ["-DDBAG_K2E_G=4"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
