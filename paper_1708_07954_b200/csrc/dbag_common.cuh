@@ -56,6 +56,33 @@ struct __align__(16) PointRec {
 };
 static_assert(sizeof(PointRec) == 64, "PointRec must be 64 B");
 
+// 256-bit global loads / stores (sm_100: LDG.E.256 / STG.E.256), 32 B aligned
+// addresses. A gather of 64 B records or 32 B consensus points by a warp costs
+// one L1 wavefront per lane and per instruction, so halving the instruction
+// count halves the L1 data-pipe work of the gather (K2 is bound by it).
+__device__ __forceinline__ void ldg256(const void* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+// read-only data (not written by the running kernel)
+__device__ __forceinline__ void ldg256_nc(const void* p, double& a, double& b, double& c,
+                                          double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(void* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+__device__ __forceinline__ PointRec load_rec256(const PointRec* p) {
+  PointRec r;
+  ldg256(p, r.x0, r.x1, r.x2, r.r0);
+  ldg256(reinterpret_cast<const double*>(p) + 4, r.r1, r.r2, r.u, r.v);
+  return r;
+}
+
 // Everything a kernel needs, passed by value (fits the 4 KB param space).
 struct DevState {
   int64_t L;       // observations == blocks (1,1)

@@ -19,10 +19,13 @@ VARIANTS = {
     "exact_batch128": ["-DDBAG_K1E_BATCH=128"],
     "exact_effort_off": ["-DDBAG_EFFORT_MAX_L=0"],
     # EXACT K1, Huber (dbag_exact.cu k_local_huber_pool): pool size / CTAs per SM
+    "hub_ls1": ["-DDBAG_HUB_LS=1"],
+    "hub_ls3": ["-DDBAG_HUB_LS=3"],
+    "hub_ls5": ["-DDBAG_HUB_LS=5"],
     "hub_q40": ["-DDBAG_HUB_Q=40", "-DDBAG_HUB_MINB=12"],
     "hub_q56": ["-DDBAG_HUB_Q=56", "-DDBAG_HUB_MINB=8"],
     "hub_q64": ["-DDBAG_HUB_Q=64", "-DDBAG_HUB_MINB=7"],
-    "k2_minb4": ["-DDBAG_K2E_MINB=4"],
+    "k2_minb3": ["-DDBAG_K2E_MINB=3"],
     # K3 exact: the streamed persistent kernel off / ring depth
     "k3_percam": ["-DDBAG_K3_STREAM_MIN_OBS=2000000000"],
     "k3_stream": ["-DDBAG_K3_STREAM_MIN_OBS=1024"],
