@@ -748,6 +748,10 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     S.record = dev_alloc<double>(pool, kRecFields + 4);
     S.metric_part = dev_alloc<double>(pool, kRecFields);
     S.work = dev_alloc<unsigned long long>(pool, 1);
+    // dbag_get_consensus's [n][3] staging, taken with the other persistent
+    // buffers so that a later handle finds it in the pool (allocated on first
+    // use it grew the pool inside the caller's timed read-back: 149 ms)
+    if (!h->sharded()) h->pack_pts = dev_alloc<double>(pool, 3 * (size_t)std::max(N, 1));
     S.effort = nullptr;
     S.order = nullptr;
     // effort-ordered K1 (launch_local): per-observation effort of the last

@@ -48,12 +48,16 @@ inline cudaError_t resident_ctas(const void* kern, int threads, size_t smem, int
 // contiguous, ascending camera = ascending block order, admm_solver.cpp:126-140).
 // 64 B = two full 32 B sectors: the local solve gathers it once per round, the
 // point consensus pass streams it.
-struct __align__(16) PointRec {
+// Sector A (bytes 0..31) = x | u: written by K1 (the copy). Sector B (32..63) =
+// r | v: written by K2 (the dual). Each kernel dirties one 32 B sector of a
+// record, so the write-back to HBM is 32 B per copy and kernel instead of 64.
+struct __align__(32) PointRec {
   double x0, x1, x2;  // local point copy x_i^j
-  double r0;          // dual r_i^j
-  double r1, r2;
-  double u, v;        // observation z (read-only)
+  double u;           // observation z (read-only)
+  double r0, r1, r2;  // dual r_i^j
+  double v;           // observation z (read-only)
 };
+constexpr int kRecX = 0, kRecU = 3, kRecR = 4, kRecV = 7;  // offsets in doubles
 static_assert(sizeof(PointRec) == 64, "PointRec must be 64 B");
 
 // 256-bit global loads / stores (sm_100: LDG.E.256 / STG.E.256), 32 B aligned
@@ -78,8 +82,8 @@ __device__ __forceinline__ void stg256(void* p, double a, double b, double c, do
 }
 __device__ __forceinline__ PointRec load_rec256(const PointRec* p) {
   PointRec r;
-  ldg256(p, r.x0, r.x1, r.x2, r.r0);
-  ldg256(reinterpret_cast<const double*>(p) + 4, r.r1, r.r2, r.u, r.v);
+  ldg256(p, r.x0, r.x1, r.x2, r.u);
+  ldg256(reinterpret_cast<const double*>(p) + 4, r.r0, r.r1, r.r2, r.v);
   return r;
 }
 
@@ -160,7 +164,10 @@ __device__ __forceinline__ void boundary_copy(const DevState& S, int64_t slot, d
   } else {
     const double* a = reinterpret_cast<const double*>(S.prec + (-2 - slot));
 #pragma unroll
-    for (int k = 0; k < 6; ++k) c[k] = a[k];
+    for (int k = 0; k < 3; ++k) {
+      c[k] = a[kRecX + k];
+      c[3 + k] = a[kRecR + k];
+    }
   }
 }
 

@@ -485,8 +485,8 @@ __global__ void k_copies(DevState S, double* lp, double* lc, double* r, double* 
   double* rec = reinterpret_cast<double*>(S.prec + S.blk_pos[b]);
   if (dir == 0) {
     for (int k = 0; k < 3; ++k) {
-      lp[3 * b + k] = rec[k];
-      r[3 * b + k] = rec[3 + k];
+      lp[3 * b + k] = rec[kRecX + k];
+      r[3 * b + k] = rec[kRecR + k];
     }
     for (int k = 0; k < 6; ++k) {
       lc[6 * b + k] = S.cam_soa[(int64_t)k * S.L + b];
@@ -494,8 +494,8 @@ __global__ void k_copies(DevState S, double* lp, double* lc, double* r, double* 
     }
   } else {
     for (int k = 0; k < 3; ++k) {
-      rec[k] = lp[3 * b + k];
-      rec[3 + k] = r[3 * b + k];
+      rec[kRecX + k] = lp[3 * b + k];
+      rec[kRecR + k] = r[3 * b + k];
     }
     for (int k = 0; k < 6; ++k) {
       S.cam_soa[(int64_t)k * S.L + b] = lc[6 * b + k];

@@ -140,8 +140,8 @@ __global__ void k_reset_state(DevState S, const double* init_pose, const double*
   const int j = S.blk_cam[b], i = S.blk_pt[b];
   double* r = reinterpret_cast<double*>(S.prec + S.blk_pos[b]);
   for (int q = 0; q < 3; ++q) {
-    r[q] = init_pts[3 * (int64_t)i + q];
-    r[3 + q] = 0.0;
+    r[kRecX + q] = init_pts[3 * (int64_t)i + q];
+    r[kRecR + q] = 0.0;
   }
   for (int q = 0; q < 6; ++q) {
     S.cam_soa[(int64_t)q * S.L + b] = init_pose[6 * (int64_t)j + q];

@@ -618,6 +618,25 @@ def test_gpu_exact_against_glibc_geometry_oracle(O, P, tmp_path):
     g.close()
 
 
+@pytest.mark.parametrize("stream", ["1", "0"])
+@pytest.mark.parametrize("config,scale,loss", [(1, 1.0, 0), (2, 0.25, 1), (3, 0.02, 0), (4, 0.01, 1)])
+def test_camera_consensus_kernels_agree(O, P, monkeypatch, stream, config, scale, loss):
+    """K3 has two kernels (dbag_exact.cu launch_camera): one CTA per camera, and
+    the streamed persistent kernel that long cameras take (producer / ordered-sum /
+    dual-worker warps). DBAG_K3_STREAM forces either on any scene; both must
+    reproduce the oracle's consensus, duals and residual maxima bit for bit
+    (admm_solver.cpp:333-357), including cameras shorter than one chunk and
+    scenes with fewer cameras than SMs."""
+    monkeypatch.setenv("DBAG_K3_STREAM", stream)
+    arrays, init, scene = config_arrays(P, config, 2, scale)
+    _, osol, g = pair(O, P, arrays, init, loss=loss, max_iters=6)
+    ot = osol.run()
+    gt = g.run()
+    assert_exact_trajectory(ot, gt)
+    assert_state_identical(osol, g)
+    g.close()
+
+
 def test_round_graph_replay_matches_direct_launches(P):
     """From the second round on, iterate/run replay the round as one CUDA graph
     (dbag_capi.cu enqueue_round). A process with DBAG_NO_GRAPH=1 launches the
