@@ -29,7 +29,6 @@ VARIANTS = {
     # K3 exact: the streamed persistent kernel off / ring depth
     "k3_percam": ["-DDBAG_K3_STREAM_MIN_OBS=2000000000"],
     "k3_stream": ["-DDBAG_K3_STREAM_MIN_OBS=1024"],
-    "k3_stream_nohint": ["-DDBAG_K3_STREAM_MIN_OBS=1024", "-DDBAG_K3S_L2HINT=0"],
     "k3_stream_p7": ["-DDBAG_K3_STREAM_MIN_OBS=1024", "-DDBAG_K3S_PROD=7"],
     # K2 exact: lanes per point
     "k2_g4": ["-DDBAG_K2E_G=4"],
