@@ -494,21 +494,22 @@ def our_arm(args, rank, world, local_rank):
     if (dom == "local" and not general and args.numerics == "exact" and args.loss == "l2"
             and args.config == 5 and world == 1):
         try:
-            t = json.load(open(os.path.join(ROOT, "profiles", "r1_k1_traffic_config5.json")))
+            t = json.load(open(os.path.join(ROOT, "profiles", "r2d_k1_traffic_config5.json")))
             traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
         except (OSError, ValueError, KeyError):
             traffic = None
     # ncu-measured FP64 pipe activity of K1 (the north star's evidence for the
     # local solves), from the committed profile of this numerics mode
     pipe = None
-    prof = {"exact": "r1_k1_exact_markstein_config5s01.txt",
+    prof = {"exact": "r2d_k1_exact_config5_full.txt",
             "fast": "r1_k1_fast_v4_config5s01.txt"}.get(args.numerics)
     if prof and not general and args.loss == "l2":
         try:
             for ln in open(os.path.join(ROOT, "profiles", prof)):
                 if ln.startswith("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"):
                     pipe = {"frac": float(ln.split()[1]) / 100.0, "source": "profiles/" + prof,
-                            "note": "ncu --set full, config 5 at scale 0.1"}
+                            "note": "ncu --set full, config 5 at " +
+                                    ("full size" if "full" in prof else "scale 0.1")}
                     break
         except (OSError, ValueError, IndexError):
             pipe = None
@@ -517,7 +518,7 @@ def our_arm(args, rank, world, local_rank):
                            if general else "k_local (K1 local solve)"), "bound": "fp64",
                 "achieved": kernels["local"]["tflops"], "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": kernels["local"]["frac_fp64"], "traffic": traffic,
-                "traffic_unit": "DRAM bytes per launch (ncu, profiles/r1_k1_traffic_config5.json)",
+                "traffic_unit": "DRAM bytes per launch (ncu, profiles/r2d_k1_traffic_config5.json)",
                 "peak_source": "measured on this device by dbag_measure_fp64_peak (DFMA probe); "
                                "MEASURED_PEAKS.json has no FP64 figure",
                 "hbm_frac_same_kernel": kernels["local"]["frac_hbm"],
