@@ -793,6 +793,8 @@ static void create_impl(dbag_solver* h, const dbag_problem_view* P, const dbag_p
     S.rho_y = o.rho_y;
     S.w_x = std::sqrt(0.5 * o.rho_x);  // IEEE sqrt: the device's sqrt() bit for bit
     S.w_y = std::sqrt(0.5 * o.rho_y);
+    S.y_x = 1.0 / o.rho_x;  // IEEE division: RN(1 / rho), the device's rcp_rn_fast bit for bit
+    S.y_y = 1.0 / o.rho_y;
     S.eps_depth = o.eps_depth;
     S.huber_delta = o.huber_delta;
     S.grad_tol = o.grad_tol;

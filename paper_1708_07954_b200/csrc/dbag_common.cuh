@@ -113,6 +113,7 @@ struct DevState {
   // options
   double rho_x, rho_y, eps_depth, huber_delta;
   double w_x, w_y;  // sqrt(0.5 * rho): the residual row weights (admm_solver.cpp:183-184)
+  double y_x, y_y;  // RN(1 / rho): the reciprocal the EXACT K1's target divisions correct (host '/')
   double grad_tol, step_tol, armijo_c, backtrack;
   int32_t inner_max_iters, lbfgs_memory, max_line_search, loss;
   // reductions

@@ -25,9 +25,6 @@ VARIANTS = {
     "hub_q40": ["-DDBAG_HUB_Q=40", "-DDBAG_HUB_MINB=12"],
     "hub_q56": ["-DDBAG_HUB_Q=56", "-DDBAG_HUB_MINB=8"],
     "hub_q64": ["-DDBAG_HUB_Q=64", "-DDBAG_HUB_MINB=7"],
-    "k1_stage": ["-DDBAG_K1E_STAGE"],
-    "k1_stage_rollt": ["-DDBAG_K1E_STAGE", "-DDBAG_K1E_ROLLT"],
-    "k1_rollt": ["-DDBAG_K1E_ROLLT"],
     "hub_fixed3": ["-DDBAG_HUB_LS_MIN=1", "-DDBAG_HUB_LS=3"],
     "hub_m20_l8": ["-DDBAG_HUB_LS_MIN=20", "-DDBAG_HUB_LS=8"],
     "k2_minb3": ["-DDBAG_K2E_MINB=3"],
