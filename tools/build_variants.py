@@ -34,6 +34,7 @@ VARIANTS = {
     "k3_stream_p7": ["-DDBAG_K3_STREAM_MIN_OBS=1024", "-DDBAG_K3S_PROD=7"],
     # K2 exact: lanes per point
     "k2_g4": ["-DDBAG_K2E_G=4"],
+    "k2_g8": ["-DDBAG_K2E_G=8"],
     # FAST K1 (dbag_local.cuh via dbag_capi.cu)
     "fast_minb3": ["-DDBAG_K1_MINB=3"],
     # generalized blocks (dbag_blocks.cu)
