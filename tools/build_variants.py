@@ -31,7 +31,8 @@ VARIANTS = {
     # K3 exact: the streamed persistent kernel off / ring depth
     "k3_percam": ["-DDBAG_K3_STREAM_MIN_OBS=2000000000"],
     "k3_stream": ["-DDBAG_K3_STREAM_MIN_OBS=1024"],
-    "k3_stream_p7": ["-DDBAG_K3_STREAM_MIN_OBS=1024", "-DDBAG_K3S_PROD=7"],
+    "k3s_p7": ["-DDBAG_K3S_PROD=7"],
+    "k3s_sl0": ["-DDBAG_K3S_SLEEP=0"],
     # K2 exact: lanes per point
     "k2_g4": ["-DDBAG_K2E_G=4"],
     "k2_g8": ["-DDBAG_K2E_G=8"],
