@@ -25,12 +25,16 @@ VARIANTS = {
     "hub_q40": ["-DDBAG_HUB_Q=40", "-DDBAG_HUB_MINB=12"],
     "hub_q56": ["-DDBAG_HUB_Q=56", "-DDBAG_HUB_MINB=8"],
     "hub_q64": ["-DDBAG_HUB_Q=64", "-DDBAG_HUB_MINB=7"],
+    "hub_u2": ["-DDBAG_HUB_UNROLL=2"],
+    "hub_u4": ["-DDBAG_HUB_UNROLL=4"],
     "hub_fixed3": ["-DDBAG_HUB_LS_MIN=1", "-DDBAG_HUB_LS=3"],
     "hub_m20_l8": ["-DDBAG_HUB_LS_MIN=20", "-DDBAG_HUB_LS=8"],
     "k2_minb3": ["-DDBAG_K2E_MINB=3"],
     # K3 exact: the streamed persistent kernel off / ring depth
     "k3_percam": ["-DDBAG_K3_STREAM_MIN_OBS=2000000000"],
     "k3_stream": ["-DDBAG_K3_STREAM_MIN_OBS=1024"],
+    "k3s_t768": ["-DDBAG_K3S_THREADS=768"],
+    "k3s_t640": ["-DDBAG_K3S_THREADS=640"],
     "k3s_p7": ["-DDBAG_K3S_PROD=7"],
     "k3s_sl0": ["-DDBAG_K3S_SLEEP=0"],
     # K2 exact: lanes per point
