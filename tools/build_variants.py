@@ -25,8 +25,6 @@ VARIANTS = {
     "hub_q40": ["-DDBAG_HUB_Q=40", "-DDBAG_HUB_MINB=12"],
     "hub_q56": ["-DDBAG_HUB_Q=56", "-DDBAG_HUB_MINB=8"],
     "hub_q64": ["-DDBAG_HUB_Q=64", "-DDBAG_HUB_MINB=7"],
-    "hub_u2": ["-DDBAG_HUB_UNROLL=2"],
-    "hub_u4": ["-DDBAG_HUB_UNROLL=4"],
     "hub_fixed3": ["-DDBAG_HUB_LS_MIN=1", "-DDBAG_HUB_LS=3"],
     "hub_m20_l8": ["-DDBAG_HUB_LS_MIN=20", "-DDBAG_HUB_LS=8"],
     "k2_minb3": ["-DDBAG_K2E_MINB=3"],
